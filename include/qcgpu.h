@@ -1,0 +1,268 @@
+/*
+ * qcgpu.h — C-ABI of the B200-native ParaQAOA hot path (libqcgpu.so).
+ *
+ * Drop-in boundary for the reference's C++ API in /root/reference/proj/include/qcut/:
+ * every entry point below replaces one reference function (cited per declaration),
+ * takes caller-owned POD buffers (host memory), and reports errors as status codes
+ * instead of exceptions. include/qcut_gpu.hpp rethrows them as the reference's
+ * exception types (errors.hpp:8-24), so callers such as pipeline.hpp:263 keep their
+ * error handling unchanged.
+ *
+ * Status codes: QC_OK 0, QC_ERR_CONFIG 1 (config_error), QC_ERR_RESOURCE 2
+ * (resource_error, including device out-of-memory), QC_ERR_IO 3 (io_error),
+ * QC_ERR_INTERNAL 4 (CUDA failure / internal). qc_last_error() returns the message
+ * of the calling thread's last failure.
+ *
+ * Amplitude buffers are interleaved complex128 (re, im) of length 2^q, basis index z
+ * with bit v = vertex v (statevector.hpp:22-23), i.e. the memory layout of
+ * std::vector<std::complex<double>>.
+ *
+ * Numerics: fp64, bit-identical to the reference's canonical (no-FMA) build on the
+ * integral-weight path (the phase LUT is built on the host with std::polar exactly
+ * as statevector.hpp:154-157; the device uses explicitly rounded mul/add, ascending
+ * RX targets and the 4096-blocked sequential expectation of statevector.hpp:48-65).
+ * Non-integral weights (statevector.hpp:162-164) use a device sincos: agreement
+ * within 1e-12 relative, not bit-exact.
+ */
+#ifndef QCGPU_H
+#define QCGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QC_OK 0
+#define QC_ERR_CONFIG 1
+#define QC_ERR_RESOURCE 2
+#define QC_ERR_IO 3
+#define QC_ERR_INTERNAL 4
+
+#define QC_ABI_VERSION 1
+
+typedef struct qc_engine qc_engine;
+
+/* graph.hpp:24-28 Edge: u < v not required on input (Graph::add_edge swaps). */
+typedef struct {
+    uint32_t u;
+    uint32_t v;
+    double w;
+} qc_edge;
+
+/* graph.hpp:32-81 Graph: vertex count + edge list (edge-list order is significant for
+ * non-integral weights, statevector.hpp:103-107). */
+typedef struct {
+    int32_t n;
+    int32_t m;
+    const qc_edge* edges;
+} qc_graph;
+
+/* qaoa.hpp:136-145 SolveOptions. */
+typedef struct {
+    int32_t top_k;      /* default 2 */
+    int32_t layers;     /* default 3 */
+    int32_t budget;     /* default 200 */
+    int32_t fold;       /* default 1 */
+    uint64_t seed;      /* default 0 */
+    uint64_t qubit_cap; /* default 20; the engine's hard cap (qc_qubit_cap) still binds */
+    double tolerance;   /* default 1e-5 */
+    int32_t threads;    /* accepted for API parity; ignored (device execution) */
+    int32_t reserved;
+} qc_solve_options;
+
+/* qaoa.hpp:147-152 SolveResult + qaoa.hpp:130-134 CandidateSet. The caller owns bits
+ * and probs (capacity >= top_k) and params (capacity 2*layers, [gammas..., betas...]). */
+typedef struct {
+    int32_t width;
+    int32_t folded;
+    int32_t count; /* entries written */
+    int32_t evals;
+    double expectation;
+    uint32_t* bits;
+    double* probs;
+    double* params;
+} qc_solve_result;
+
+/* merge.hpp:19-25 CandidatePool, flattened: level i has counts[i] entries of width
+ * widths[i], concatenated in bits. */
+typedef struct {
+    int32_t levels;
+    const int32_t* widths;
+    const int32_t* counts;
+    const uint32_t* bits;
+} qc_pool;
+
+/* partition.hpp:22-34 PartitionResult reduced to what the merge reads: piece i covers
+ * global ids [first[i], last[i]] and overlaps piece i+1 in exactly one vertex. */
+typedef struct {
+    int32_t pieces;
+    const int32_t* first;
+    const int32_t* last;
+} qc_chain;
+
+/* merge.hpp:85-91 MergeOptions (eval: 0 kFullGraph, 1 kIncremental). */
+typedef struct {
+    int32_t start_level;
+    int32_t workers;
+    int32_t incremental;
+    int32_t halve_symmetry;
+    double path_budget;
+} qc_merge_options;
+
+/* merge.hpp:333-338 ChainedMergeOptions. */
+typedef struct {
+    int64_t window;
+    int64_t window_leaves;
+    int32_t workers;
+    int32_t halve_symmetry;
+} qc_chained_merge_options;
+
+/* merge.hpp:93-97 MergeResult; assignment: caller-owned, n bytes (0/1). */
+typedef struct {
+    double best_value;
+    uint64_t candidates_evaluated;
+    uint8_t* assignment;
+} qc_merge_result;
+
+/* pipeline.hpp:36-68 RunConfig (hot-path subset; graph given explicitly). */
+typedef struct {
+    int32_t qubit_cap;        /* 20 */
+    int32_t subgraphs;        /* 0 = derive_subgraph_count */
+    int32_t top_k;            /* 2; 0 = every class */
+    int32_t start_level;      /* 1 */
+    int32_t layers;           /* 3 */
+    int32_t budget;           /* 200 */
+    uint64_t seed;            /* 0 */
+    int32_t fold;             /* 1 */
+    int32_t halve_symmetry;   /* 0 */
+    int32_t partition_mode;   /* 0 balanced, 1 tail-remainder */
+    int32_t merge_incremental;/* 1 */
+    int32_t merge_mode;       /* 0 auto, 1 level, 2 windowed */
+    int32_t shard_index;      /* this process's shard of the subgraphs (multi-GPU) */
+    int32_t shard_count;      /* 1 = single GPU */
+    int32_t reserved;
+    double path_budget;       /* 1e9 */
+    double nm_tolerance;      /* 1e-5 */
+} qc_run_config;
+
+/* pipeline.hpp ExperimentReport: the fields the hot path produces. */
+typedef struct {
+    double cut;
+    uint64_t candidates_evaluated;
+    double partition_s, qaoa_s, merge_s, total_s;
+    int32_t subgraphs;
+    int32_t windowed;
+    uint64_t evals; /* objective evaluations across all subgraphs */
+} qc_run_report;
+
+/* ---- engine ------------------------------------------------------------------- */
+int qc_engine_create(int device, qc_engine** out);
+void qc_engine_destroy(qc_engine* e);
+const char* qc_last_error(void);
+int qc_abi_version(void);
+/* statevector.hpp:20 kQubitCap analogue: the largest subgraph the engine simulates. */
+int qc_qubit_cap(void);
+/* Kernel launches issued by this engine since creation (bench evidence). */
+uint64_t qc_engine_launches(const qc_engine* e);
+/* Device bytes of stored-state / scratch the engine may use; 0 = automatic. */
+int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
+
+/* ---- statevector.hpp ---------------------------------------------------------- */
+/* statevector.hpp:75-111 CostTable: out[z] = C(z) for z < 2^n. */
+int qc_cost_table(qc_engine* e, const qc_graph* g, int cap, double* out, int* integral,
+                  double* max_value);
+/* statevector.hpp:134-143 plus_state. */
+int qc_plus_state(qc_engine* e, int q, int cap, double* amps);
+/* statevector.hpp:146-171 apply_cost_layer (in place on a host state). */
+int qc_apply_cost_layer(qc_engine* e, int q, double* amps, const qc_graph* g, double gamma);
+/* statevector.hpp:189-221 apply_mixer_layer (in place). */
+int qc_apply_mixer_layer(qc_engine* e, int q, double* amps, double beta);
+/* statevector.hpp:224-235 expectation. */
+int qc_expectation(qc_engine* e, int q, const double* amps, const qc_graph* g, double* out);
+/* statevector.hpp:237-241 norm_sq. */
+int qc_norm_sq(qc_engine* e, int q, const double* amps, double* out);
+
+/* ---- qaoa.hpp ----------------------------------------------------------------- */
+/* qaoa.hpp:27-38 linear_ramp. */
+int qc_linear_ramp(int p, double* gammas, double* betas);
+/* qaoa.hpp:59-73 run_ansatz (+ statevector.hpp:224 expectation); amps/expectation
+ * optional (NULL). */
+int qc_run_ansatz(qc_engine* e, const qc_graph* g, int p, const double* gammas,
+                  const double* betas, double* amps, double* expectation);
+/* qaoa.hpp:89-91 objective, batched: for each point k, expectation of run_ansatz on
+ * graphs[index[k]] at params[k*2p .. k*2p+2p) (packed [gammas..., betas...]). */
+int qc_eval_batch(qc_engine* e, const qc_graph* graphs, int n_graphs, int p, int n_points,
+                  const int32_t* index, const double* params, double* expectation);
+/* qaoa.hpp:85-117 optimize_parameters for n graphs at once (lockstep ask/tell
+ * Nelder-Mead; graph i uses seeds[i]). params: n x 2p. Optional trace (NULL): the
+ * (x, f) of every objective call, trace_x n x budget x 2p, trace_f n x budget. */
+int qc_optimize_batch(qc_engine* e, const qc_graph* graphs, int n, int p, int budget,
+                      const uint64_t* seeds, double tolerance, double* params,
+                      double* expectation, int32_t* evals, double* trace_x, double* trace_f);
+/* qaoa.hpp:158-193 top_candidates on a host state. */
+int qc_top_candidates(qc_engine* e, int q, const double* amps, int top_k, int fold,
+                      uint32_t* bits, double* probs);
+/* qaoa.hpp:198-216 solve_subgraph. */
+int qc_solve_subgraph(qc_engine* e, const qc_graph* g, const qc_solve_options* opt,
+                      qc_solve_result* res);
+/* pipeline.hpp:239-263: solve_subgraph for n independent subgraphs (opts[i] each) in
+ * one batched device pass. */
+int qc_solve_batch(qc_engine* e, const qc_graph* graphs, int n, const qc_solve_options* opts,
+                   qc_solve_result* results);
+
+/* ---- ask/tell optimisers (host only, no device) --------------------------------
+ * The engine's lockstep optimiser exposed for callers with their own objective.
+ * qc_simplex: nelder_mead.hpp:29-120 nelder_mead_minimize (initial step 0.2,
+ * coefficients 1/2/0.5/0.5); qc_optimizer: qaoa.hpp:85-117 optimize_parameters
+ * (objective = -<C>; ramp start, seeded restarts). ask() yields the next point to
+ * evaluate (done=1 once the run is over); tell() consumes its objective value. */
+typedef struct qc_simplex qc_simplex;
+int qc_simplex_create(const double* x0, int n, int max_evals, double tolerance,
+                      qc_simplex** out);
+int qc_simplex_ask(qc_simplex* s, double* x, int* done);
+int qc_simplex_tell(qc_simplex* s, double f);
+int qc_simplex_result(const qc_simplex* s, double* x, double* value, int* evals, int* converged);
+void qc_simplex_destroy(qc_simplex* s);
+
+typedef struct qc_optimizer qc_optimizer;
+int qc_optimizer_create(int p, int budget, uint64_t seed, double tolerance, qc_optimizer** out);
+int qc_optimizer_ask(qc_optimizer* o, double* x, int* done);
+int qc_optimizer_tell(qc_optimizer* o, double f);
+int qc_optimizer_result(const qc_optimizer* o, double* params, double* expectation, int* evals);
+void qc_optimizer_destroy(qc_optimizer* o);
+
+/* ---- merge.hpp ---------------------------------------------------------------- */
+/* merge.hpp:280-331 level_aware_merge. */
+int qc_level_merge(qc_engine* e, const qc_pool* pool, const qc_graph* g, const qc_chain* chain,
+                   const qc_merge_options* opt, qc_merge_result* res);
+/* merge.hpp:345-412 chained_merge. */
+int qc_chained_merge(qc_engine* e, const qc_pool* pool, const qc_graph* g,
+                     const qc_chain* chain, const qc_chained_merge_options* opt,
+                     qc_merge_result* res);
+
+/* ---- pipeline.hpp (hot-path stages) ------------------------------------------- */
+/* pipeline.hpp:111-124 schedule rounds are replaced by one batched solve; this runs
+ * partition (partition.hpp:111) -> QAOA stage (pipeline.hpp:219-296) -> merge
+ * (pipeline.hpp:298-334) for graph g and fills report + assignment (n bytes '0'/'1'
+ * plus NUL). With shard_count > 1 only the QAOA stage of shard shard_index runs and
+ * qc_run_pipeline returns after writing the shard's solve records (see
+ * qc_shard_solve); the merge then runs on the gathered records (qc_merge_records). */
+int qc_run_pipeline(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
+                    qc_run_report* report, char* assignment);
+
+/* Multi-GPU: fixed-size solve records for the NCCL gather.
+ * record_bytes(top_k_cap, layers) gives the size of one record; qc_shard_solve solves
+ * subgraphs [begin, end) of the partition of g and writes end-begin records;
+ * qc_merge_records merges M records (all shards, in subgraph order). */
+int64_t qc_record_bytes(int top_k_cap, int layers);
+int qc_shard_range(int M, int shard_index, int shard_count, int32_t* begin, int32_t* end);
+int qc_shard_solve(qc_engine* e, const qc_graph* g, const qc_run_config* cfg, int32_t begin,
+                   int32_t end, void* records, int32_t* subgraphs);
+int qc_merge_records(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
+                     const void* records, int32_t M, qc_run_report* report, char* assignment);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCGPU_H */

@@ -105,12 +105,12 @@ class _Lib:
             raise FileNotFoundError(path)
         self.path = path
         self.lib = C.CDLL(path)
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _call(self, name, *args):
-        rc = self.lib[self.prefix + name](*args)
+        rc = getattr(self.lib, self.prefix + name)(*args)
         if rc != 0:
-            msg = self.lib[self.prefix + "last_error"]().decode()
+            msg = getattr(self.lib, self.prefix + "last_error")().decode()
             raise _ERR.get(rc, OracleError)(rc, msg)
 
     # --- graph / partition ---------------------------------------------------

@@ -1,0 +1,792 @@
+// Engine: device memory, batched objective evaluation, lockstep optimisation, solve,
+// and the statevector.hpp / qaoa.hpp entry points of the C-ABI (include/qcgpu.h).
+// Host code is compiled with -ffp-contract=off: the phase LUT (std::polar), cos/sin(beta)
+// and every Nelder-Mead expression round exactly like the reference's canonical build.
+#include "qc_engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <numbers>
+#include <unordered_set>
+
+#include "qc_nm.hpp"
+
+namespace qcg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaErrorMemoryAllocation) {
+        (void)cudaGetLastError();
+        resource_error(std::string("device out of memory (") + what + ")");
+    }
+    internal_error(std::string("CUDA error: ") + cudaGetErrorString(e) + " in " + what + " at " +
+                   file + ":" + std::to_string(line));
+}
+
+void* DevBuf::get(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes > cap) {
+        release();
+        QC_CUDA(cudaMalloc(&p, bytes));
+        cap = bytes;
+    }
+    return p;
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+void* HostBuf::get(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (bytes > cap) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        QC_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+        cap = bytes;
+    }
+    return p;
+}
+HostBuf::~HostBuf() {
+    if (p) cudaFreeHost(p);
+}
+
+// graph.hpp:37-50 Graph::add_edge validation; statevector.hpp:83-89 integrality.
+HostGraph load_graph(const qc_graph* g) {
+    if (!g) config_error("null graph");
+    if (g->n < 0) config_error("negative vertex count");
+    if (g->m < 0) config_error("negative edge count");
+    if (g->m > 0 && !g->edges) config_error("null edge list");
+    HostGraph h;
+    h.n = g->n;
+    h.u.reserve(static_cast<size_t>(g->m));
+    h.v.reserve(static_cast<size_t>(g->m));
+    h.w.reserve(static_cast<size_t>(g->m));
+    std::unordered_set<uint64_t> keys;
+    keys.reserve(static_cast<size_t>(g->m) * 2);
+    for (int i = 0; i < g->m; ++i) {
+        uint32_t u = g->edges[i].u, v = g->edges[i].v;
+        const double w = g->edges[i].w;
+        if (u >= static_cast<uint32_t>(g->n) || v >= static_cast<uint32_t>(g->n))
+            config_error("edge endpoint out of range: (" + std::to_string(u) + "," +
+                         std::to_string(v) + ") with n=" + std::to_string(g->n));
+        if (u == v) config_error("self-loop rejected at vertex " + std::to_string(u));
+        if (w < 0.0 || std::isnan(w)) config_error("negative or NaN edge weight rejected");
+        if (u > v) std::swap(u, v);
+        const uint64_t key = static_cast<uint64_t>(u) * static_cast<uint64_t>(g->n) + v;
+        if (!keys.insert(key).second)
+            config_error("duplicate edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
+        h.u.push_back(u);
+        h.v.push_back(v);
+        h.w.push_back(w);
+        h.total += w;
+        if (w != std::floor(w) || w < 0.0) h.integral = false;
+    }
+    if (h.total > 65535.0) h.integral = false;
+    return h;
+}
+
+}  // namespace qcg
+
+using namespace qcg;
+
+// ---------------------------------------------------------------------------
+// engine
+// ---------------------------------------------------------------------------
+std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool allow_sym,
+                                         bool unit_cost) {
+    std::vector<DevGraph> dg(hg.size());
+    size_t bytes = 0, ebytes = 0;
+    std::vector<size_t> off(hg.size()), eoff(hg.size());
+    for (size_t i = 0; i < hg.size(); ++i) {
+        DevGraph& d = dg[i];
+        d.q = hg[i].n;
+        d.sym = allow_sym && d.q >= 2;
+        d.Q = d.sym ? d.q - 1 : d.q;
+        d.integral = hg[i].integral;
+        d.unit_cost = unit_cost;
+        d.lut_len = d.integral ? static_cast<int>(hg[i].total) + 1 : 0;
+        off[i] = bytes;
+        if (!unit_cost) {
+            const size_t entries = size_t{1} << d.Q;
+            bytes += (d.integral ? 2 : 8) * entries;
+            bytes = (bytes + 255) & ~size_t{255};
+        }
+        eoff[i] = ebytes;
+        ebytes += hg[i].u.size() * 16 + 256;
+    }
+    char* base = static_cast<char*>(tables.get(bytes));
+    if (unit_cost) return dg;
+    char* ebase = static_cast<char*>(edges.get(ebytes));
+    char* hbase = static_cast<char*>(hstage.get(ebytes));
+    for (size_t i = 0; i < hg.size(); ++i) {
+        const size_t m = hg[i].u.size();
+        char* h = hbase + eoff[i];
+        std::memcpy(h, hg[i].u.data(), m * 4);
+        std::memcpy(h + m * 4, hg[i].v.data(), m * 4);
+        std::memcpy(h + m * 8, hg[i].w.data(), m * 8);
+    }
+    QC_CUDA(cudaMemcpyAsync(ebase, hbase, ebytes, cudaMemcpyHostToDevice, stream));
+    for (size_t i = 0; i < hg.size(); ++i) {
+        DevGraph& d = dg[i];
+        const size_t m = hg[i].u.size();
+        char* de = ebase + eoff[i];
+        if (d.integral)
+            d.lev = reinterpret_cast<uint16_t*>(base + off[i]);
+        else
+            d.val = reinterpret_cast<double*>(base + off[i]);
+        launches += launch_levels(reinterpret_cast<uint32_t*>(de), reinterpret_cast<uint32_t*>(de + m * 4),
+                                  reinterpret_cast<double*>(de + m * 8), static_cast<int>(m), d.Q,
+                                  d.integral, d.lev, d.val, stream);
+    }
+    // the host staging buffer is reused by the next upload: wait for this copy
+    QC_CUDA(cudaStreamSynchronize(stream));
+    return dg;
+}
+
+size_t qc_engine::max_slots(int Q, bool onchip) const {
+    const size_t N = size_t{1} << Q;
+    const size_t per = N * 16 + (onchip ? 0 : N * 8 + (N / 4096 + 2) * 16) + 64;
+    size_t budget = mem_budget;
+    if (budget == 0) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = size_t{8} << 30;
+        budget = static_cast<size_t>(static_cast<double>(fr + states.cap + fbuf.cap) * 0.6);
+    }
+    size_t s = budget / per;
+    if (s < 1) s = 1;
+    if (onchip) s = std::min<size_t>(s, 1u << 16);
+    return s;
+}
+
+double2* qc_engine::slot_state(int q, bool sym, int k) {
+    const int Q = sym ? q - 1 : q;
+    return static_cast<double2*>(states.p) + (static_cast<size_t>(k) << Q);
+}
+
+void qc_engine::sync() { QC_CUDA(cudaStreamSynchronize(stream)); }
+
+void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
+                           uint32_t flags, double* out) {
+    if (n <= 0) return;
+    const DevGraph& g0 = dg[static_cast<size_t>(pts[0].g)];
+    const ChainPlan plan = plan_chain(g0.q, g0.sym);
+    const size_t N = size_t{1} << plan.Q;
+    auto* st = static_cast<double2*>(states.get(static_cast<size_t>(n) * N * 16));
+    double* fb = nullptr;
+    if (!plan.onchip && (flags & F_EXPECT))
+        fb = static_cast<double*>(fbuf.get(static_cast<size_t>(n) * N * 8));
+    const size_t pps = partials_per_slot(plan);
+    auto* part = static_cast<double*>(partials.get(static_cast<size_t>(n) * pps * 8 + 8));
+    auto* od = static_cast<double*>(outd.get(static_cast<size_t>(n) * 8));
+
+    // staging: [SlotDesc n][LayerParam n*p][LUT entries]
+    size_t lut_total = 0;
+    for (int k = 0; k < n; ++k) {
+        const DevGraph& d = dg[static_cast<size_t>(pts[k].g)];
+        if (d.integral && !d.unit_cost)
+            for (int l = 0; l < p; ++l)
+                if (pts[k].x[l] != 0.0) lut_total += static_cast<size_t>(d.lut_len);
+    }
+    const size_t o_lp = (static_cast<size_t>(n) * sizeof(SlotDesc) + 255) & ~size_t{255};
+    const size_t o_lut =
+        (o_lp + static_cast<size_t>(n) * static_cast<size_t>(std::max(p, 1)) * sizeof(LayerParam) + 255) &
+        ~size_t{255};
+    const size_t bytes = o_lut + lut_total * 16;
+    char* h = static_cast<char*>(hstage.get(bytes));
+    char* d = static_cast<char*>(stage.get(bytes));
+    auto* hs = reinterpret_cast<SlotDesc*>(h);
+    auto* hl = reinterpret_cast<LayerParam*>(h + o_lp);
+    auto* hlut = reinterpret_cast<double*>(h + o_lut);
+    size_t lut_pos = 0;
+    const double amp0 = 1.0 / std::sqrt(static_cast<double>(size_t{1} << g0.q));  // :141
+    for (int k = 0; k < n; ++k) {
+        const DevGraph& dgk = dg[static_cast<size_t>(pts[k].g)];
+        SlotDesc& s = hs[k];
+        s.state = st + static_cast<size_t>(k) * N;
+        s.fbuf = fb ? fb + static_cast<size_t>(k) * N : nullptr;
+        s.lev = dgk.unit_cost ? nullptr : dgk.lev;
+        s.val = dgk.unit_cost ? nullptr : dgk.val;
+        s.amp0 = amp0;
+        s.layer_base = k * p;
+        s.pad = 0;
+        for (int l = 0; l < p; ++l) {
+            LayerParam& L = hl[static_cast<size_t>(k) * static_cast<size_t>(p) + static_cast<size_t>(l)];
+            const double gamma = pts[k].x[l];
+            const double beta = pts[k].x[p + l];
+            // statevector.hpp:192 (host libm, exactly like the reference)
+            L.c = std::cos(beta);
+            L.s = std::sin(beta);
+            L.mix = (L.s == 0.0 && L.c == 1.0) ? 0 : 1;
+            L.phase = gamma == 0.0 ? 0 : 1;  // :149
+            L.gamma = gamma;
+            L.lut = nullptr;
+            if (L.phase && dgk.integral && !dgk.unit_cost) {
+                // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c)
+                double* dst = hlut + 2 * lut_pos;
+                for (int c = 0; c < dgk.lut_len; ++c) {
+                    const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
+                    dst[2 * c] = z.real();
+                    dst[2 * c + 1] = z.imag();
+                }
+                L.lut = reinterpret_cast<const double2*>(d + o_lut) + lut_pos;
+                lut_pos += static_cast<size_t>(dgk.lut_len);
+            }
+        }
+    }
+    QC_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+    launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
+                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, part, od,
+                             stream);
+    if (flags & F_EXPECT) {
+        auto* ho = static_cast<double*>(hout.get(static_cast<size_t>(n) * 8));
+        QC_CUDA(cudaMemcpyAsync(ho, od, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, stream));
+        QC_CUDA(cudaStreamSynchronize(stream));
+        std::memcpy(out, ho, static_cast<size_t>(n) * 8);
+    } else {
+        QC_CUDA(cudaStreamSynchronize(stream));
+    }
+}
+
+void qc_engine::eval(const std::vector<DevGraph>& dg, const std::vector<EvalPoint>& pts, int p,
+                     double* out) {
+    // group by qubit count (one launch chain per group and chunk)
+    std::map<int, std::vector<int>> by_q;
+    for (size_t k = 0; k < pts.size(); ++k) by_q[dg[static_cast<size_t>(pts[k].g)].q].push_back(static_cast<int>(k));
+    std::vector<EvalPoint> buf;
+    std::vector<double> res;
+    for (auto& [q, idx] : by_q) {
+        const DevGraph& g0 = dg[static_cast<size_t>(pts[static_cast<size_t>(idx[0])].g)];
+        const ChainPlan plan = plan_chain(q, g0.sym);
+        const size_t cap = max_slots(plan.Q, plan.onchip);
+        for (size_t b = 0; b < idx.size(); b += cap) {
+            const size_t e = std::min(idx.size(), b + cap);
+            buf.clear();
+            for (size_t k = b; k < e; ++k) buf.push_back(pts[static_cast<size_t>(idx[k])]);
+            res.assign(buf.size(), 0.0);
+            eval_chunk(dg, buf.data(), static_cast<int>(buf.size()), p, F_INIT | F_EXPECT,
+                       res.data());
+            for (size_t k = b; k < e; ++k) out[idx[k]] = res[k - b];
+        }
+    }
+}
+
+namespace qcg {
+
+std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph>& dg,
+                                        const std::vector<int>& layers,
+                                        const std::vector<int>& budget,
+                                        const std::vector<uint64_t>& seeds,
+                                        const std::vector<double>& tol,
+                                        std::vector<std::vector<double>>* trace_x,
+                                        std::vector<std::vector<double>>* trace_f) {
+    const size_t n = dg.size();
+    std::vector<AngleOptimizer> opt(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (budget[i] < 1) config_error("optimizer budget must be positive");  // qaoa.hpp:88
+        if (layers[i] < 1) config_error("layer count must be positive");      // qaoa.hpp:28
+        opt[i].start(layers[i], budget[i], seeds[i], tol[i]);
+    }
+    // one lockstep step: every live optimiser asks one point; points grouped by p
+    std::vector<EvalPoint> pts;
+    std::vector<int> who;
+    std::vector<double> vals;
+    std::map<int, std::vector<size_t>> by_p;
+    for (;;) {
+        by_p.clear();
+        for (size_t i = 0; i < n; ++i)
+            if (!opt[i].done()) by_p[layers[i]].push_back(i);
+        if (by_p.empty()) break;
+        for (auto& [p, ids] : by_p) {
+            pts.clear();
+            for (size_t i : ids) pts.push_back({static_cast<int>(i), opt[i].point().data()});
+            vals.assign(pts.size(), 0.0);
+            e->eval(dg, pts, p, vals.data());
+            for (size_t k = 0; k < ids.size(); ++k) {
+                const size_t i = ids[k];
+                const double f = -vals[k];  // qaoa.hpp:90
+                if (trace_x) {
+                    const auto& x = opt[i].point();
+                    (*trace_x)[i].insert((*trace_x)[i].end(), x.begin(), x.end());
+                    (*trace_f)[i].push_back(f);
+                }
+                opt[i].tell(f);
+            }
+        }
+    }
+    std::vector<OptimizeOut> out(n);
+    for (size_t i = 0; i < n; ++i) {
+        out[i].params = opt[i].params;
+        out[i].expectation = opt[i].expectation();
+        out[i].evals = opt[i].evals;
+    }
+    return out;
+}
+
+std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
+                                  const std::vector<qc_solve_options>& opts) {
+    const size_t n = hg.size();
+    for (size_t i = 0; i < n; ++i) {  // qaoa.hpp:199-203, then :88, :28, :162-165
+        const int q = hg[i].n;
+        if (q < 1) config_error("cannot solve an empty subgraph");
+        const uint64_t cap = std::min<uint64_t>(opts[i].qubit_cap, static_cast<uint64_t>(kMaxQubits));
+        if (static_cast<uint64_t>(q) > cap)
+            resource_error("subgraph has " + std::to_string(q) + " vertices, over the " +
+                           std::to_string(cap) + "-qubit cap");
+        if (opts[i].budget < 1) config_error("optimizer budget must be positive");
+        if (opts[i].layers < 1) config_error("layer count must be positive");
+        const uint64_t classes = opts[i].fold ? (uint64_t{1} << (q - 1)) : (uint64_t{1} << q);
+        if (opts[i].top_k < 1 || static_cast<uint64_t>(opts[i].top_k) > classes)
+            config_error("top_k must lie in [1, " + std::to_string(classes) + "] for " +
+                         std::to_string(q) + " qubits" + (opts[i].fold ? " (folded)" : ""));
+    }
+    const std::vector<DevGraph> dg = e->prepare(hg, true);
+    std::vector<int> layers(n), budget(n);
+    std::vector<uint64_t> seeds(n);
+    std::vector<double> tol(n);
+    for (size_t i = 0; i < n; ++i) {
+        layers[i] = opts[i].layers;
+        budget[i] = opts[i].budget;
+        seeds[i] = opts[i].seed;
+        tol[i] = opts[i].tolerance;
+    }
+    const auto best = optimize_batch(e, dg, layers, budget, seeds, tol, nullptr, nullptr);
+
+    // final circuit at the best angles (qaoa.hpp:208) + top-K (qaoa.hpp:211)
+    std::vector<SolveOut> out(n);
+    std::map<std::pair<int, int>, std::vector<size_t>> groups;  // (q, p)
+    for (size_t i = 0; i < n; ++i) groups[{hg[i].n, layers[i]}].push_back(i);
+    for (auto& [key, ids] : groups) {
+        const int q = key.first, p = key.second;
+        const ChainPlan plan = plan_chain(q, dg[ids[0]].sym);
+        const size_t cap = e->max_slots(plan.Q, plan.onchip);
+        for (size_t b = 0; b < ids.size(); b += cap) {
+            const size_t end = std::min(ids.size(), b + cap);
+            std::vector<EvalPoint> pts;
+            for (size_t k = b; k < end; ++k) pts.push_back({static_cast<int>(ids[k]), best[ids[k]].params.data()});
+            e->eval_chunk(dg, pts.data(), static_cast<int>(pts.size()), p, F_INIT | F_STATE_OUT,
+                          nullptr);
+            for (size_t k = b; k < end; ++k) {
+                const size_t i = ids[k];
+                const int K = opts[i].top_k;
+                const bool fold = opts[i].fold != 0;
+                const size_t sb = topk_scratch_bytes(q, fold, K);
+                void* scratch = e->topk_scratch.get(sb);
+                char* ob = static_cast<char*>(e->topk_out.get(static_cast<size_t>(K) * 12 + 64));
+                auto* d_bits = reinterpret_cast<uint32_t*>(ob);
+                auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(K) * 4 + 15) & ~size_t{15}));
+                e->launches += launch_topk(e->slot_state(q, dg[i].sym, static_cast<int>(k - b)), q,
+                                           dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream);
+                SolveOut& r = out[i];
+                r.width = q;
+                r.folded = fold;
+                r.bits.resize(static_cast<size_t>(K));
+                r.probs.resize(static_cast<size_t>(K));
+                QC_CUDA(cudaMemcpyAsync(r.bits.data(), d_bits, static_cast<size_t>(K) * 4,
+                                        cudaMemcpyDeviceToHost, e->stream));
+                QC_CUDA(cudaMemcpyAsync(r.probs.data(), d_probs, static_cast<size_t>(K) * 8,
+                                        cudaMemcpyDeviceToHost, e->stream));
+                e->sync();
+                r.params = best[i].params;
+                r.expectation = best[i].expectation;
+                r.evals = best[i].evals;
+            }
+        }
+    }
+    return out;
+}
+
+}  // namespace qcg
+
+// ---------------------------------------------------------------------------
+// C-ABI: engine + statevector.hpp + qaoa.hpp
+// ---------------------------------------------------------------------------
+namespace {
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return QC_OK;
+    } catch (const qcg::Error& e) {
+        qcg::set_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        qcg::set_error("host out of memory");
+        return QC_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        qcg::set_error(e.what());
+        return QC_ERR_INTERNAL;
+    }
+}
+
+void check_engine(qc_engine* e) {
+    if (!e) config_error("null engine");
+    QC_CUDA(cudaSetDevice(e->device));
+}
+
+// Run a FULL-mode single-state chain on a host state (statevector.hpp layer calls).
+void full_state_op(qc_engine* e, int q, double* amps, const DevGraph& dg, int p,
+                   const double* x, uint32_t flags, double* out_expect) {
+    const ChainPlan plan = plan_chain(q, false);
+    const size_t N = size_t{1} << q;
+    auto* st = static_cast<double2*>(e->states.get(N * 16));
+    if (!(flags & F_INIT)) {
+        auto* h = static_cast<double*>(e->hstage.get(N * 16));
+        std::memcpy(h, amps, N * 16);
+        QC_CUDA(cudaMemcpyAsync(st, h, N * 16, cudaMemcpyHostToDevice, e->stream));
+        QC_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    std::vector<DevGraph> v{dg};
+    EvalPoint pt{0, x};
+    double ex = 0.0;
+    if (p == 0 && !plan.onchip) internal_error("layerless chain on a multi-pass state");
+    e->eval_chunk(v, &pt, 1, p, flags, &ex);
+    if (out_expect) *out_expect = ex;
+    if (flags & F_STATE_OUT) {
+        auto* h = static_cast<double*>(e->hout.get(N * 16));
+        QC_CUDA(cudaMemcpyAsync(h, e->states.p, N * 16, cudaMemcpyDeviceToHost, e->stream));
+        QC_CUDA(cudaStreamSynchronize(e->stream));
+        std::memcpy(amps, h, N * 16);
+    }
+}
+
+int check_q(int q, int cap_max) {
+    if (q < 1) config_error("state needs at least one qubit");
+    if (q > cap_max) resource_error("state rejected: " + std::to_string(q) + " qubits exceeds cap " + std::to_string(cap_max));
+    return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qc_last_error(void) { return qcg::last_error(); }
+int qc_abi_version(void) { return QC_ABI_VERSION; }
+int qc_qubit_cap(void) { return kMaxQubits; }
+uint64_t qc_engine_launches(const qc_engine* e) { return e ? e->launches : 0; }
+
+int qc_engine_create(int device, qc_engine** out) {
+    return guarded([&] {
+        if (!out) config_error("null output pointer");
+        int count = 0;
+        QC_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            resource_error("CUDA device " + std::to_string(device) + " not available");
+        QC_CUDA(cudaSetDevice(device));
+        auto* e = new qc_engine();
+        e->device = device;
+        QC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        *out = e;
+    });
+}
+
+void qc_engine_destroy(qc_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    cudaStreamSynchronize(e->stream);
+    cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes) {
+    return guarded([&] {
+        check_engine(e);
+        e->mem_budget = bytes;
+    });
+}
+
+int qc_cost_table(qc_engine* e, const qc_graph* g, int cap, double* out, int* integral,
+                  double* max_value) {
+    return guarded([&] {
+        check_engine(e);
+        const HostGraph hg = load_graph(g);
+        if (hg.n < 1) config_error("cost table needs at least one vertex");
+        if (hg.n > cap || hg.n > kMaxQubits)
+            resource_error("cost table rejected: " + std::to_string(hg.n) + " qubits exceeds cap " +
+                           std::to_string(std::min(cap, kMaxQubits)));
+        const auto dg = e->prepare({hg}, false);
+        const size_t N = size_t{1} << hg.n;
+        double mx = 0.0;
+        if (dg[0].integral) {
+            std::vector<uint16_t> lev(N);
+            QC_CUDA(cudaMemcpyAsync(lev.data(), dg[0].lev, N * 2, cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+            for (size_t z = 0; z < N; ++z) {
+                out[z] = static_cast<double>(lev[z]);
+                mx = std::max(mx, out[z]);
+            }
+        } else {
+            QC_CUDA(cudaMemcpyAsync(out, dg[0].val, N * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+            for (size_t z = 0; z < N; ++z) mx = std::max(mx, out[z]);
+        }
+        if (integral) *integral = dg[0].integral ? 1 : 0;
+        if (max_value) *max_value = mx;
+    });
+}
+
+int qc_plus_state(qc_engine* e, int q, int cap, double* amps) {
+    return guarded([&] {
+        check_engine(e);
+        check_q(q, std::min(cap, kMaxQubits));
+        if (q > 12) {
+            // |+> of a multi-pass state: the first pass of a zero-angle layer writes it
+            HostGraph hg;
+            hg.n = q;
+            const auto dg = e->prepare({hg}, false, true);
+            const double x[2] = {0.0, 0.0};
+            full_state_op(e, q, amps, dg[0], 1, x, F_INIT | F_STATE_OUT, nullptr);
+            return;
+        }
+        HostGraph hg;
+        hg.n = q;
+        const auto dg = e->prepare({hg}, false, true);
+        full_state_op(e, q, amps, dg[0], 0, nullptr, F_INIT | F_STATE_OUT, nullptr);
+    });
+}
+
+int qc_apply_cost_layer(qc_engine* e, int q, double* amps, const qc_graph* g, double gamma) {
+    return guarded([&] {
+        check_engine(e);
+        const HostGraph hg = load_graph(g);
+        if (hg.n < 1) config_error("cost table needs at least one vertex");
+        if (hg.n > kMaxQubits) resource_error("cost table rejected: qubits exceeds cap");
+        if (hg.n != q) config_error("state and cost table disagree on qubit count");
+        if (gamma == 0.0) return;  // statevector.hpp:149
+        const auto dg = e->prepare({hg}, false);
+        const double x[2] = {gamma, 0.0};  // beta 0 => mixer skipped exactly
+        full_state_op(e, q, amps, dg[0], 1, x, F_STATE_OUT, nullptr);
+    });
+}
+
+int qc_apply_mixer_layer(qc_engine* e, int q, double* amps, double beta) {
+    return guarded([&] {
+        check_engine(e);
+        if (q < 1) config_error("mixer on empty state");
+        if (q > kMaxQubits) resource_error("state exceeds the engine cap");
+        HostGraph hg;
+        hg.n = q;
+        const auto dg = e->prepare({hg}, false, true);
+        const double x[2] = {0.0, beta};
+        full_state_op(e, q, amps, dg[0], 1, x, F_STATE_OUT, nullptr);
+    });
+}
+
+int qc_expectation(qc_engine* e, int q, const double* amps, const qc_graph* g, double* out) {
+    return guarded([&] {
+        check_engine(e);
+        const HostGraph hg = load_graph(g);
+        if (hg.n < 1) config_error("cost table needs at least one vertex");
+        if (hg.n > kMaxQubits) resource_error("cost table rejected: qubits exceeds cap");
+        if (hg.n != q) config_error("state and cost table disagree on qubit count");
+        const auto dg = e->prepare({hg}, false);
+        const double x[2] = {0.0, 0.0};
+        std::vector<double> tmp(amps, amps + 2 * (size_t{1} << q));
+        // a zero-angle layer is an exact identity; its last pass emits the terms
+        full_state_op(e, q, tmp.data(), dg[0], q > 12 ? 1 : 0, x, F_EXPECT, out);
+    });
+}
+
+int qc_norm_sq(qc_engine* e, int q, const double* amps, double* out) {
+    return guarded([&] {
+        check_engine(e);
+        check_q(q, kMaxQubits);
+        HostGraph hg;
+        hg.n = q;
+        const auto dg = e->prepare({hg}, false, true);
+        const double x[2] = {0.0, 0.0};
+        std::vector<double> tmp(amps, amps + 2 * (size_t{1} << q));
+        full_state_op(e, q, tmp.data(), dg[0], q > 12 ? 1 : 0, x, F_EXPECT, out);
+    });
+}
+
+int qc_linear_ramp(int p, double* gammas, double* betas) {
+    return guarded([&] {
+        if (p < 1) config_error("layer count must be positive");
+        const auto x = linear_ramp_packed(p);
+        for (int l = 0; l < p; ++l) {
+            gammas[l] = x[static_cast<size_t>(l)];
+            betas[l] = x[static_cast<size_t>(p + l)];
+        }
+    });
+}
+
+int qc_run_ansatz(qc_engine* e, const qc_graph* g, int p, const double* gammas,
+                  const double* betas, double* amps, double* expectation) {
+    return guarded([&] {
+        check_engine(e);
+        const HostGraph hg = load_graph(g);
+        if (hg.n < 1) config_error("cost table needs at least one vertex");
+        if (hg.n > kMaxQubits) resource_error("cost table rejected: qubits exceeds cap");
+        if (p < 0) config_error("gamma and beta schedules must have equal length");
+        const auto dg = e->prepare({hg}, true);
+        std::vector<double> x(static_cast<size_t>(2 * std::max(p, 1)), 0.0);
+        for (int l = 0; l < p; ++l) {
+            x[static_cast<size_t>(l)] = gammas[l];
+            x[static_cast<size_t>(p + l)] = betas[l];
+        }
+        const ChainPlan plan = plan_chain(hg.n, dg[0].sym);
+        if (p == 0 && !plan.onchip) {
+            // |+> with no layers: the expectation of the uniform state
+            std::vector<double> tmp(2 * (size_t{1} << hg.n));
+            full_state_op(e, hg.n, tmp.data(), e->prepare({hg}, false, true)[0], 1,
+                          std::vector<double>{0.0, 0.0}.data(), F_INIT | F_STATE_OUT, nullptr);
+            if (amps) std::memcpy(amps, tmp.data(), tmp.size() * 8);
+            if (expectation) {
+                const auto dgf = e->prepare({hg}, false);
+                full_state_op(e, hg.n, tmp.data(), dgf[0], 1, std::vector<double>{0.0, 0.0}.data(),
+                              F_EXPECT, expectation);
+            }
+            return;
+        }
+        EvalPoint pt{0, x.data()};
+        double ex = 0.0;
+        e->eval_chunk(dg, &pt, 1, p, F_INIT | F_EXPECT | (amps ? F_STATE_OUT : 0u), &ex);
+        if (expectation) *expectation = ex;
+        if (amps) {
+            const int q = hg.n;
+            const size_t N = size_t{1} << plan.Q;
+            std::vector<double> half(2 * N);
+            QC_CUDA(cudaMemcpyAsync(half.data(), e->states.p, N * 16, cudaMemcpyDeviceToHost, e->stream));
+            e->sync();
+            const size_t full = (size_t{1} << q) - 1;
+            for (size_t z = 0; z <= full; ++z) {  // a_{~z} == a_z (complement symmetry)
+                const size_t i = (!dg[0].sym || z < N) ? z : (full ^ z);
+                amps[2 * z] = half[2 * i];
+                amps[2 * z + 1] = half[2 * i + 1];
+            }
+        }
+    });
+}
+
+int qc_eval_batch(qc_engine* e, const qc_graph* graphs, int n_graphs, int p, int n_points,
+                  const int32_t* index, const double* params, double* expectation) {
+    return guarded([&] {
+        check_engine(e);
+        if (p < 1) config_error("layer count must be positive");
+        std::vector<HostGraph> hg;
+        for (int i = 0; i < n_graphs; ++i) {
+            hg.push_back(load_graph(&graphs[i]));
+            if (hg.back().n < 1) config_error("cost table needs at least one vertex");
+            if (hg.back().n > kMaxQubits) resource_error("graph exceeds the engine qubit cap");
+        }
+        const auto dg = e->prepare(hg, true);
+        std::vector<EvalPoint> pts(static_cast<size_t>(n_points));
+        for (int k = 0; k < n_points; ++k) {
+            if (index[k] < 0 || index[k] >= n_graphs) config_error("point graph index out of range");
+            pts[static_cast<size_t>(k)] = {index[k], params + static_cast<size_t>(k) * 2 * static_cast<size_t>(p)};
+        }
+        e->eval(dg, pts, p, expectation);
+    });
+}
+
+int qc_optimize_batch(qc_engine* e, const qc_graph* graphs, int n, int p, int budget,
+                      const uint64_t* seeds, double tolerance, double* params, double* expectation,
+                      int32_t* evals, double* trace_x, double* trace_f) {
+    return guarded([&] {
+        check_engine(e);
+        std::vector<HostGraph> hg;
+        for (int i = 0; i < n; ++i) {
+            hg.push_back(load_graph(&graphs[i]));
+            if (hg.back().n < 1) config_error("cost table needs at least one vertex");
+            if (hg.back().n > kMaxQubits) resource_error("graph exceeds the engine qubit cap");
+        }
+        if (budget < 1) config_error("optimizer budget must be positive");
+        if (p < 1) config_error("layer count must be positive");
+        const auto dg = e->prepare(hg, true);
+        std::vector<int> L(static_cast<size_t>(n), p), B(static_cast<size_t>(n), budget);
+        std::vector<uint64_t> S(seeds, seeds + n);
+        std::vector<double> T(static_cast<size_t>(n), tolerance);
+        std::vector<std::vector<double>> tx(static_cast<size_t>(n)), tf(static_cast<size_t>(n));
+        const auto out = optimize_batch(e, dg, L, B, S, T, trace_x ? &tx : nullptr,
+                                        trace_x ? &tf : nullptr);
+        for (int i = 0; i < n; ++i) {
+            const auto& o = out[static_cast<size_t>(i)];
+            std::memcpy(params + static_cast<size_t>(i) * 2 * p, o.params.data(), 16 * static_cast<size_t>(p));
+            expectation[i] = o.expectation;
+            evals[i] = o.evals;
+            if (trace_x) {
+                const size_t stride_x = static_cast<size_t>(budget) * 2 * p;
+                std::fill(trace_x + i * stride_x, trace_x + (i + 1) * stride_x, 0.0);
+                std::fill(trace_f + static_cast<size_t>(i) * budget, trace_f + static_cast<size_t>(i + 1) * budget, 0.0);
+                std::memcpy(trace_x + i * stride_x, tx[static_cast<size_t>(i)].data(),
+                            std::min(tx[static_cast<size_t>(i)].size(), stride_x) * 8);
+                std::memcpy(trace_f + static_cast<size_t>(i) * budget, tf[static_cast<size_t>(i)].data(),
+                            std::min<size_t>(tf[static_cast<size_t>(i)].size(), static_cast<size_t>(budget)) * 8);
+            }
+        }
+    });
+}
+
+int qc_top_candidates(qc_engine* e, int q, const double* amps, int top_k, int fold,
+                      uint32_t* bits, double* probs) {
+    return guarded([&] {
+        check_engine(e);
+        if (q < 1) config_error("cannot rank candidates of an empty state");
+        if (q > 32) resource_error("candidate bits limited to 32 qubits");
+        if (q > kMaxQubits) resource_error("state exceeds the engine qubit cap");
+        const uint64_t classes = fold ? (uint64_t{1} << (q - 1)) : (uint64_t{1} << q);
+        if (top_k < 1 || static_cast<uint64_t>(top_k) > classes)
+            config_error("top_k must lie in [1, " + std::to_string(classes) + "] for " +
+                         std::to_string(q) + " qubits" + (fold ? " (folded)" : ""));
+        const size_t N = size_t{1} << q;
+        auto* st = static_cast<double2*>(e->states.get(N * 16));
+        auto* h = static_cast<double*>(e->hstage.get(N * 16));
+        std::memcpy(h, amps, N * 16);
+        QC_CUDA(cudaMemcpyAsync(st, h, N * 16, cudaMemcpyHostToDevice, e->stream));
+        void* scratch = e->topk_scratch.get(topk_scratch_bytes(q, fold != 0, top_k));
+        char* ob = static_cast<char*>(e->topk_out.get(static_cast<size_t>(top_k) * 12 + 64));
+        auto* d_bits = reinterpret_cast<uint32_t*>(ob);
+        auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(top_k) * 4 + 15) & ~size_t{15}));
+        e->launches += launch_topk(st, q, false, fold != 0, top_k, scratch, d_bits, d_probs, e->stream);
+        QC_CUDA(cudaMemcpyAsync(bits, d_bits, static_cast<size_t>(top_k) * 4, cudaMemcpyDeviceToHost, e->stream));
+        QC_CUDA(cudaMemcpyAsync(probs, d_probs, static_cast<size_t>(top_k) * 8, cudaMemcpyDeviceToHost, e->stream));
+        e->sync();
+    });
+}
+
+static void fill_result(const SolveOut& s, qc_solve_result* r) {
+    r->width = s.width;
+    r->folded = s.folded ? 1 : 0;
+    r->count = static_cast<int32_t>(s.bits.size());
+    r->evals = s.evals;
+    r->expectation = s.expectation;
+    if (r->bits) std::memcpy(r->bits, s.bits.data(), s.bits.size() * 4);
+    if (r->probs) std::memcpy(r->probs, s.probs.data(), s.probs.size() * 8);
+    if (r->params) std::memcpy(r->params, s.params.data(), s.params.size() * 8);
+}
+
+int qc_solve_subgraph(qc_engine* e, const qc_graph* g, const qc_solve_options* opt,
+                      qc_solve_result* res) {
+    return guarded([&] {
+        check_engine(e);
+        if (!opt || !res) config_error("null options/result");
+        const auto out = solve_batch(e, {load_graph(g)}, {*opt});
+        fill_result(out[0], res);
+    });
+}
+
+int qc_solve_batch(qc_engine* e, const qc_graph* graphs, int n, const qc_solve_options* opts,
+                   qc_solve_result* results) {
+    return guarded([&] {
+        check_engine(e);
+        std::vector<HostGraph> hg;
+        std::vector<qc_solve_options> o(opts, opts + n);
+        for (int i = 0; i < n; ++i) hg.push_back(load_graph(&graphs[i]));
+        const auto out = solve_batch(e, hg, o);
+        for (int i = 0; i < n; ++i) fill_result(out[static_cast<size_t>(i)], &results[i]);
+    });
+}
+
+}  // extern "C"

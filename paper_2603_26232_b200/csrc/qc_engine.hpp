@@ -1,0 +1,109 @@
+// Engine internals shared by qc_engine.cpp and qc_pipeline.cpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/qcgpu.h"
+#include "qc_internal.hpp"
+
+namespace qcg {
+
+// Validated host copy of a qcut::Graph (graph.hpp:37-50 add_edge rules) plus the
+// CostTable integrality rule (statevector.hpp:83-89).
+struct HostGraph {
+    int n = 0;
+    std::vector<uint32_t> u, v;
+    std::vector<double> w;
+    bool integral = true;
+    double total = 0.0;
+};
+HostGraph load_graph(const qc_graph* g);
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes);
+    void release();
+    ~DevBuf() { release(); }
+};
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes);
+    ~HostBuf();
+};
+
+// Device cut table of one graph: 2^Q entries (levels or values).
+struct DevGraph {
+    int q = 0, Q = 0;
+    bool sym = false;
+    bool integral = true;
+    bool unit_cost = false;  // norm_sq: cost 1 everywhere
+    int lut_len = 0;
+    uint16_t* lev = nullptr;
+    double* val = nullptr;
+};
+
+struct EvalPoint {
+    int g;            // graph index
+    const double* x;  // packed [gammas..., betas...]
+};
+
+}  // namespace qcg
+
+struct qc_engine {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    uint64_t mem_budget = 0;
+    qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out;
+    qcg::HostBuf hstage, hout;
+
+    // Build the device cut tables of graphs (sym: half state) into `tables`.
+    std::vector<qcg::DevGraph> prepare(const std::vector<qcg::HostGraph>& hg, bool allow_sym,
+                                       bool unit_cost = false);
+    // Evaluate points sharing (q, p) in chunks; out[k] = <C> of point k.
+    // flags: qcg::F_* (F_STATE_OUT keeps each chunk's states for `on_chunk`).
+    size_t max_slots(int Q, bool onchip) const;
+    void eval_chunk(const std::vector<qcg::DevGraph>& dg, const qcg::EvalPoint* pts, int n, int p,
+                    uint32_t flags, double* out);
+    void eval(const std::vector<qcg::DevGraph>& dg, const std::vector<qcg::EvalPoint>& pts, int p,
+              double* out);
+    double2* slot_state(int q, bool sym, int k);
+    void sync();
+};
+
+namespace qcg {
+// Lockstep batched optimisation (qaoa.hpp:85-117 for many graphs).
+struct OptimizeOut {
+    std::vector<double> params;
+    double expectation = 0.0;
+    int evals = 0;
+};
+std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph>& dg,
+                                        const std::vector<int>& layers,
+                                        const std::vector<int>& budget,
+                                        const std::vector<uint64_t>& seeds,
+                                        const std::vector<double>& tol,
+                                        std::vector<std::vector<double>>* trace_x,
+                                        std::vector<std::vector<double>>* trace_f);
+
+struct SolveOut {
+    int width = 0;
+    bool folded = true;
+    std::vector<uint32_t> bits;
+    std::vector<double> probs;
+    std::vector<double> params;
+    double expectation = 0.0;
+    int evals = 0;
+};
+std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
+                                  const std::vector<qc_solve_options>& opts);
+
+void set_error(const std::string& msg);
+
+}  // namespace qcg

@@ -1,0 +1,92 @@
+// Internal declarations shared by the host C++ (g++) and the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace qcg {
+
+// Status-coded exception; the C-ABI layer maps it to QC_ERR_* (qcgpu.h).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void config_error(const std::string& m) { throw Error(1, m); }
+[[noreturn]] inline void resource_error(const std::string& m) { throw Error(2, m); }
+[[noreturn]] inline void internal_error(const std::string& m) { throw Error(4, m); }
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define QC_CUDA(x)                                                        \
+    do {                                                                  \
+        cudaError_t err_ = (x);                                           \
+        if (err_ != cudaSuccess) ::qcg::cuda_fail(err_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+// Largest simulated subgraph (stored half-state 2^25 amplitudes = 512 MiB fp64).
+constexpr int kMaxQubits = 30;
+constexpr int kLowBits = 12;   // pass A tile: 2^12 contiguous stored amplitudes
+constexpr int kBlock = 4096;   // statevector.hpp:53 blocked_sum block
+
+// ---------------------------------------------------------------------------
+// Device-side descriptors. One "slot" = one state buffer evaluating one point.
+// ---------------------------------------------------------------------------
+struct SlotDesc {
+    double2* state;        // 2^Q stored amplitudes
+    double* fbuf;          // 2^Q per-amplitude expectation terms (scratch)
+    const uint16_t* lev;   // integral cut levels, 2^Q entries (or null)
+    const double* val;     // fractional cut values, 2^Q entries (or null)
+    double amp0;           // 1/sqrt(2^q)
+    int32_t layer_base;    // first LayerParam of this slot
+    int32_t pad;
+};
+
+struct LayerParam {
+    const double2* lut;    // integral: host-built std::polar(1,-gamma*c) table (device copy)
+    double gamma;          // fractional path: per-amplitude phase angle factor
+    double c, s;           // cos(beta), sin(beta) (host libm, statevector.hpp:192)
+    int32_t phase;         // gamma != 0 (statevector.hpp:149)
+    int32_t mix;           // !(s == 0 && c == 1) (statevector.hpp:193)
+};
+
+// Mode flags for a launch chain.
+enum : uint32_t {
+    F_INIT = 1u,        // first layer starts from |+> (no state read)
+    F_EXPECT = 2u,      // compute the blocked expectation after the last layer
+    F_STATE_OUT = 4u,   // final state must be written back
+    F_SYM = 8u,         // half-state storage (complement symmetry), else full state
+};
+
+// One high (gather) pass: 3 column bits (0,1,2) + 8 tile bits.
+struct HighPass {
+    uint32_t mask[8];   // tile bit masks (single bit, or ALL for the mirror pseudo-bit)
+    int32_t kind[8];    // 0 batch (no op), 1 RX target, 2 mirror (target q-1 in SYM mode)
+    uint32_t freemask;  // stored-index bits enumerated by the tile index
+};
+
+struct ChainPlan {
+    int Q;                         // stored index bits
+    bool sym;
+    bool onchip;                   // Q <= 12: whole state per CTA
+    std::vector<HighPass> high;    // passes after pass A (bits >= 12)
+};
+ChainPlan plan_chain(int q, bool sym);
+
+// Launchers (qc_kernels.cu). All asynchronous on `stream`; return #kernels launched.
+int launch_levels(const uint32_t* d_eu, const uint32_t* d_ev, const double* d_ew, int m,
+                  int Q, bool integral, uint16_t* d_lev, double* d_val, cudaStream_t stream);
+int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
+                 int n_slots, int p, uint32_t flags, double* d_partials, double* d_out,
+                 cudaStream_t stream);
+size_t partials_per_slot(const ChainPlan& plan);
+
+// Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,
+// ordered by (prob desc, lex asc) (qaoa.hpp:179-182). d_scratch sized by topk_scratch_bytes.
+size_t topk_scratch_bytes(int q, bool fold, int k);
+int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
+                uint32_t* d_bits, double* d_probs, cudaStream_t stream);
+
+}  // namespace qcg

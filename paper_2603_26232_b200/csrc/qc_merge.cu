@@ -1,0 +1,791 @@
+// GPU merge scoring (merge.hpp:280-331 level_aware_merge, merge.hpp:345-412
+// chained_merge), sm_100a.
+//
+// Both merges are sequences of exhaustive "window" searches over compatible candidate
+// chains (level mode = one window over all levels). A leaf is a tuple of pool entries,
+// one per level, where entry i+1's bit 0 equals entry i's last bit (merge.hpp:55-58).
+// The best leaf maximises the score; ties go to the lexicographically smallest
+// assignment (merge.hpp:166-173). Because pieces are ascending contiguous vertex
+// ranges, that order is the lexicographic order of per-level lex_less_mask ranks, so
+// the engine enumerates every window's leaves in lex-DFS order (per-level candidate
+// lists sorted by bit-reversed value) and breaks ties by the smaller leaf index.
+//
+// Scoring:
+//   * integral weights (the ER/unit-weight configs): every summation order is exact, so
+//     the score is a sum of per-level unary tables and per-level-pair tables
+//     (edges bucketed by the levels of their endpoints; merge.hpp:103-113 groups the same
+//     edges by max level) — O(levels) lookups per leaf instead of O(edges);
+//   * fractional weights: the reference's floating-point association is reproduced
+//     exactly (incremental: acc + bucket sums in edge-list order, merge.hpp:115-120,
+//     182-184; full: cut_value in edge-list order at every leaf).
+//
+// Every window runs on the device back to back (no host round trip): unary tables
+// from the fixed prefix, search, block reduction, commit of the winner into the
+// device-resident assignment; the next window's seam bit is read on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <array>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "qc_internal.hpp"
+#include "qc_merge.hpp"
+
+namespace qcg {
+
+namespace {
+
+constexpr int kSearchThreads = 128;
+constexpr int kMaxL = 64;  // per-thread stacks (local memory)
+
+struct WinLevel {
+    int32_t count;        // pool entries
+    int32_t bits_off;     // into entry bits (pool order)
+    int32_t list_off[3];  // lex-sorted entry indices: parity 0, parity 1, all
+    int32_t list_len[3];
+    int32_t first;        // global id of local vertex 0
+    int32_t width;
+    int32_t u_off;        // unary table offset (count entries)
+    int32_t pair_base;    // index into pair_off for (this level, j = s .. this-1)
+    int32_t bucket_off;   // exact path: edges of this level's bucket
+    int32_t bucket_len;
+    int32_t fixed_off;    // fixed-prefix edges (integral path) for this level
+    int32_t fixed_len;
+    uint64_t nsub[2];     // leaves of levels [this, end) given incoming parity
+};
+
+struct XEdge {  // exact path edge with precomputed endpoint levels
+    uint32_t u, v;
+    double w;
+    int32_t lu, lv;
+};
+
+struct FixedEdge {  // v_hi local index k in its level, v_lo global id, integral weight
+    int32_t k;
+    int32_t u;
+    int64_t w;
+};
+
+struct SearchArgs {
+    const WinLevel* lv;       // L levels
+    const uint32_t* bits;     // entry bits
+    const int32_t* lists;     // lex lists
+    const int64_t* utab;      // unary tables (integral)
+    const int64_t* ptab;      // pair tables (integral)
+    const int32_t* pair_off;  // offsets of pair tables
+    const XEdge* xedges;      // exact path buckets
+    const XEdge* all_edges;   // full-graph scoring (edge-list order)
+    int32_t m_all;
+    const uint8_t* fixed;     // device assignment (fixed prefix)
+    const int32_t* first_of_level;  // all levels (global)
+    int32_t s;                // first level of the window (global index)
+    int32_t L;
+    int32_t need_mode;        // 2 free, 3 halve (bit0 == 0), -1 read from fixed[first[s]]
+    int32_t integral;
+    int32_t full_graph;       // exact path: score with cut_value at leaves
+    int32_t leaves_per_thread;
+    const double* base_acc;   // device acc of fixed prefix (exact path)
+    const int64_t* base_iacc; // device acc (integral path)
+    uint64_t* blk_idx;        // per-block best leaf index
+    double* blk_val;          // per-block best value (exact path / integral as double)
+    int64_t* blk_ival;
+};
+
+__device__ __forceinline__ int entry_bit(const SearchArgs& A, const WinLevel& L, int e, int k) {
+    return (A.bits[L.bits_off + e] >> k) & 1u;
+}
+
+__device__ __forceinline__ int need_parity(const SearchArgs& A) {
+    if (A.need_mode >= 0) return A.need_mode;
+    return A.fixed[A.first_of_level[A.s]];
+}
+
+// list index for a level given incoming parity / need code
+__device__ __forceinline__ int list_sel(int need) { return need == 2 ? 2 : (need == 3 ? 0 : need); }
+
+template <bool INTEGRAL>
+__device__ __forceinline__ void better(bool& has, int64_t& bi, double& bv, uint64_t& bidx,
+                                       int64_t iv, double v, uint64_t idx) {
+    if (INTEGRAL) {
+        if (!has || iv > bi || (iv == bi && idx < bidx)) {
+            has = true;
+            bi = iv;
+            bidx = idx;
+        }
+    } else {
+        if (!has || v > bv || (v == bv && idx < bidx)) {
+            has = true;
+            bv = v;
+            bidx = idx;
+        }
+    }
+}
+
+// bit of global vertex x for the current tuple (exact path)
+__device__ __forceinline__ int vertex_bit(const SearchArgs& A, const int* c, int lvl, uint32_t x) {
+    if (lvl < A.s) return A.fixed[x];
+    const WinLevel& L = A.lv[lvl - A.s];
+    return entry_bit(A, L, c[lvl - A.s], static_cast<int>(x) - L.first);
+}
+
+template <bool INTEGRAL>
+__global__ void __launch_bounds__(kSearchThreads) k_search(SearchArgs A, uint64_t total_bound) {
+    const int L = A.L;
+    const int need0 = need_parity(A);
+    // total leaves for this need
+    uint64_t T = 0;
+    {
+        const WinLevel& l0 = A.lv[0];
+        const int sel = list_sel(need0);
+        for (int r = 0; r < l0.list_len[sel]; ++r) {
+            const int e = A.lists[l0.list_off[sel] + r];
+            const int out = entry_bit(A, l0, e, l0.width - 1);
+            T += (L > 1) ? A.lv[1].nsub[out] : 1;
+        }
+    }
+    const uint64_t t = static_cast<uint64_t>(blockIdx.x) * kSearchThreads + threadIdx.x;
+    const uint64_t idx0 = t * static_cast<uint64_t>(A.leaves_per_thread);
+    bool has = false;
+    int64_t bi = 0;
+    double bv = 0.0;
+    uint64_t bidx = 0;
+
+    if (idx0 < T) {
+        int r[kMaxL], c[kMaxL], sel[kMaxL];
+        int64_t ips[kMaxL];
+        double dps[kMaxL];
+        // decode idx0
+        uint64_t rem = idx0;
+        int need = need0;
+        for (int i = 0; i < L; ++i) {
+            const WinLevel& lv = A.lv[i];
+            sel[i] = list_sel(need);
+            const int32_t* lst = A.lists + lv.list_off[sel[i]];
+            int rr = 0;
+            for (;; ++rr) {
+                const int e = lst[rr];
+                const int out = entry_bit(A, lv, e, lv.width - 1);
+                const uint64_t cnt = (i + 1 < L) ? A.lv[i + 1].nsub[out] : 1;
+                if (rem < cnt) break;
+                rem -= cnt;
+            }
+            r[i] = rr;
+            c[i] = lst[rr];
+            need = entry_bit(A, lv, c[i], lv.width - 1);
+        }
+        auto score_level = [&](int i) {
+            const WinLevel& lv = A.lv[i];
+            if (INTEGRAL) {
+                int64_t v = (i ? ips[i - 1] : 0) + A.utab[lv.u_off + c[i]];
+                for (int j = 0; j < i; ++j) {
+                    const int po = A.pair_off[lv.pair_base + j];
+                    if (po >= 0) v += A.ptab[po + c[i] * A.lv[j].count + c[j]];
+                }
+                ips[i] = v;
+            } else if (!A.full_graph) {
+                double g = 0.0;
+                const XEdge* es = A.xedges + lv.bucket_off;
+                for (int k = 0; k < lv.bucket_len; ++k) {
+                    const XEdge ed = es[k];
+                    if (vertex_bit(A, c, ed.lu, ed.u) != vertex_bit(A, c, ed.lv, ed.v))
+                        g = __dadd_rn(g, ed.w);
+                }
+                dps[i] = __dadd_rn(i ? dps[i - 1] : *A.base_acc, g);
+            }
+        };
+        for (int i = 0; i < L; ++i) score_level(i);
+        uint64_t idx = idx0;
+        const uint64_t idx_end = min(T, idx0 + static_cast<uint64_t>(A.leaves_per_thread));
+        for (;;) {
+            if (INTEGRAL) {
+                better<true>(has, bi, bv, bidx, ips[L - 1], 0.0, idx);
+            } else if (A.full_graph) {
+                double v = 0.0;
+                for (int k = 0; k < A.m_all; ++k) {
+                    const XEdge ed = A.all_edges[k];
+                    if (vertex_bit(A, c, ed.lu, ed.u) != vertex_bit(A, c, ed.lv, ed.v))
+                        v = __dadd_rn(v, ed.w);
+                }
+                better<false>(has, bi, bv, bidx, 0, v, idx);
+            } else {
+                better<false>(has, bi, bv, bidx, 0, dps[L - 1], idx);
+            }
+            if (++idx >= idx_end) break;
+            // odometer
+            int i = L - 1;
+            for (;;) {
+                const WinLevel& lv = A.lv[i];
+                if (++r[i] < lv.list_len[sel[i]]) break;
+                r[i] = 0;
+                --i;  // never underflows: idx < T guarantees a successor exists
+            }
+            for (int k = i; k < L; ++k) {
+                const WinLevel& lv = A.lv[k];
+                if (k > i) {
+                    const int inpar = entry_bit(A, A.lv[k - 1], c[k - 1], A.lv[k - 1].width - 1);
+                    sel[k] = inpar;
+                    r[k] = 0;
+                }
+                c[k] = A.lists[lv.list_off[sel[k]] + r[k]];
+                score_level(k);
+            }
+        }
+    }
+    // block reduction: (value desc, idx asc)
+    __shared__ int64_t s_i[kSearchThreads];
+    __shared__ double s_v[kSearchThreads];
+    __shared__ uint64_t s_x[kSearchThreads];
+    __shared__ int s_h[kSearchThreads];
+    s_i[threadIdx.x] = bi;
+    s_v[threadIdx.x] = bv;
+    s_x[threadIdx.x] = bidx;
+    s_h[threadIdx.x] = has ? 1 : 0;
+    __syncthreads();
+    for (int off = kSearchThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            const int o = threadIdx.x + off;
+            if (s_h[o]) {
+                bool take;
+                if (!s_h[threadIdx.x])
+                    take = true;
+                else if (INTEGRAL)
+                    take = s_i[o] > s_i[threadIdx.x] ||
+                           (s_i[o] == s_i[threadIdx.x] && s_x[o] < s_x[threadIdx.x]);
+                else
+                    take = s_v[o] > s_v[threadIdx.x] ||
+                           (s_v[o] == s_v[threadIdx.x] && s_x[o] < s_x[threadIdx.x]);
+                if (take) {
+                    s_i[threadIdx.x] = s_i[o];
+                    s_v[threadIdx.x] = s_v[o];
+                    s_x[threadIdx.x] = s_x[o];
+                    s_h[threadIdx.x] = 1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        A.blk_idx[blockIdx.x] = s_h[0] ? s_x[0] : ~uint64_t{0};
+        A.blk_val[blockIdx.x] = s_v[0];
+        A.blk_ival[blockIdx.x] = s_i[0];
+    }
+    (void)total_bound;
+}
+
+// Reduce block bests, decode the winning leaf, write its pieces into the device
+// assignment, advance the accumulated value and the leaf counter.
+__global__ void k_commit(SearchArgs A, int n_blocks, uint64_t* leaves_total, int* dead_end,
+                         double* acc, int64_t* iacc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int L = A.L;
+    const int need0 = need_parity(A);
+    uint64_t T = 0;
+    {
+        const WinLevel& l0 = A.lv[0];
+        const int sel = list_sel(need0);
+        for (int r = 0; r < l0.list_len[sel]; ++r) {
+            const int e = A.lists[l0.list_off[sel] + r];
+            const int out = entry_bit(A, l0, e, l0.width - 1);
+            T += (L > 1) ? A.lv[1].nsub[out] : 1;
+        }
+    }
+    if (T == 0) {
+        *dead_end = 1;
+        return;
+    }
+    *leaves_total += T;
+    int best = -1;
+    for (int b = 0; b < n_blocks; ++b) {
+        if (A.blk_idx[b] == ~uint64_t{0}) continue;
+        if (best < 0) {
+            best = b;
+            continue;
+        }
+        const bool take =
+            A.integral ? (A.blk_ival[b] > A.blk_ival[best] ||
+                          (A.blk_ival[b] == A.blk_ival[best] && A.blk_idx[b] < A.blk_idx[best]))
+                       : (A.blk_val[b] > A.blk_val[best] ||
+                          (A.blk_val[b] == A.blk_val[best] && A.blk_idx[b] < A.blk_idx[best]));
+        if (take) best = b;
+    }
+    if (best < 0) {
+        *dead_end = 1;
+        return;
+    }
+    uint64_t rem = A.blk_idx[best];
+    int need = need0;
+    for (int i = 0; i < L; ++i) {
+        const WinLevel& lv = A.lv[i];
+        const int32_t* lst = A.lists + lv.list_off[list_sel(need)];
+        int e = 0;
+        for (int rr = 0;; ++rr) {
+            e = lst[rr];
+            const int out = entry_bit(A, lv, e, lv.width - 1);
+            const uint64_t cnt = (i + 1 < L) ? A.lv[i + 1].nsub[out] : 1;
+            if (rem < cnt) break;
+            rem -= cnt;
+        }
+        const uint32_t b = A.bits[lv.bits_off + e];
+        for (int k = 0; k < lv.width; ++k) const_cast<uint8_t*>(A.fixed)[lv.first + k] = (b >> k) & 1u;
+        need = (b >> (lv.width - 1)) & 1u;
+    }
+    if (A.integral)
+        *iacc = A.blk_ival[best];
+    else
+        *acc = A.blk_val[best];
+}
+
+// Unary tables of the window's levels: intra-level table + edges to the fixed prefix.
+// One block per level; W0[k]/W1[k] = weight from local vertex k to fixed vertices on
+// side 0/1 (exact integer sums), then U[a] = intra[a] + sum_k (bit_a(k) ? W0 : W1).
+__global__ void k_unary(SearchArgs A, const int64_t* __restrict__ intra,
+                        const FixedEdge* __restrict__ fixed_edges, int64_t* __restrict__ utab) {
+    __shared__ unsigned long long W[2][32];
+    const WinLevel& lv = A.lv[blockIdx.x];
+    if (threadIdx.x < 64) W[threadIdx.x >> 5][threadIdx.x & 31] = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < lv.fixed_len; k += blockDim.x) {
+        const FixedEdge fe = fixed_edges[lv.fixed_off + k];
+        atomicAdd(&W[A.fixed[fe.u]][fe.k], static_cast<unsigned long long>(fe.w));
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < lv.count; a += blockDim.x) {
+        const uint32_t b = A.bits[lv.bits_off + a];
+        int64_t u = intra[lv.u_off + a];
+        for (int k = 0; k < lv.width; ++k)
+            u += static_cast<int64_t>(((b >> k) & 1u) ? W[0][k] : W[1][k]);
+        utab[lv.u_off + a] = u;
+    }
+}
+
+// Pair / intra tables: one block per group, thread per table entry, loop over the
+// group's edges (exact integer sums).
+struct PairGroup {
+    int32_t hi, lo;        // global levels (lo == hi: intra)
+    int32_t out_off;       // table offset
+    int32_t e_off, e_len;  // edges (v_hi local k, v_lo local k2, w)
+};
+struct PairEdge {
+    int32_t khi, klo;
+    int64_t w;
+};
+
+__global__ void k_pair_tables(const PairGroup* __restrict__ groups, const PairEdge* __restrict__ pe,
+                              const uint32_t* __restrict__ bits, const int32_t* __restrict__ bits_off,
+                              const int32_t* __restrict__ counts, int64_t* __restrict__ out) {
+    const PairGroup g = groups[blockIdx.x];
+    const int ch = counts[g.hi];
+    const int cl = g.lo == g.hi ? 1 : counts[g.lo];
+    for (int t = threadIdx.x; t < ch * cl; t += blockDim.x) {
+        const int a = t / cl, b = t % cl;
+        const uint32_t ba = bits[bits_off[g.hi] + a];
+        const uint32_t bb = g.lo == g.hi ? ba : bits[bits_off[g.lo] + b];
+        int64_t s = 0;
+        for (int k = 0; k < g.e_len; ++k) {
+            const PairEdge e = pe[g.e_off + k];
+            if ((((ba >> e.khi) ^ (bb >> e.klo)) & 1u) != 0) s += e.w;
+        }
+        out[g.out_off + t] = s;
+    }
+}
+
+// Integral re-score of the final assignment (cut_value, merge.hpp:327,:408).
+__global__ void k_cut_int(const uint32_t* __restrict__ eu, const uint32_t* __restrict__ ev,
+                          const double* __restrict__ ew, long long m, const uint8_t* __restrict__ a,
+                          unsigned long long* __restrict__ out) {
+    unsigned long long s = 0;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < m;
+         k += (long long)gridDim.x * blockDim.x)
+        if (a[eu[k]] != a[ev[k]]) s += static_cast<unsigned long long>(ew[k]);
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_down_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+template <typename T>
+T* dalloc(std::vector<void*>& keep, size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    QC_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    keep.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <typename T>
+T* dupload(std::vector<void*>& keep, const std::vector<T>& h, cudaStream_t st) {
+    T* d = dalloc<T>(keep, h.size());
+    if (!h.empty()) QC_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    return d;
+}
+
+uint32_t brev_w(uint32_t b) {
+    uint32_t r = 0;
+    for (int i = 0; i < 32; ++i) r |= ((b >> i) & 1u) << (31 - i);
+    return r;
+}
+
+}  // namespace
+
+// merge.hpp:122-141 check_pool_matches
+void check_pool(const MergeInput& in) {
+    const int M = in.levels;
+    if (in.pieces < 1) config_error("merge needs at least one subgraph");
+    if (M != in.pieces)
+        config_error("pool has " + std::to_string(M) + " levels for " + std::to_string(in.pieces) +
+                     " subgraphs");
+    long long covered = 0;
+    for (int i = 0; i < M; ++i) {
+        const int piece = in.last[i] - in.first[i] + 1;
+        if (in.widths[i] < 1 || in.widths[i] != piece)
+            config_error("pool level " + std::to_string(i) + " width " + std::to_string(in.widths[i]) +
+                         " does not match subgraph size " + std::to_string(piece));
+        if (in.counts[i] == 0) config_error("pool level " + std::to_string(i) + " is empty");
+        covered += piece;
+    }
+    if (covered != static_cast<long long>(in.n) + M - 1)
+        config_error("subgraphs do not cover the graph as a chain");
+}
+
+double estimate_paths(const int32_t* counts, int M, bool halve) {
+    if (M < 1) config_error("empty candidate pool");
+    double est = static_cast<double>(counts[0]);
+    if (halve) est /= 2.0;
+    for (int i = 1; i < M; ++i) est *= static_cast<double>(counts[i]) / 2.0;
+    return est;
+}
+
+MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
+                      cudaStream_t st, uint64_t* launches) {
+    const int M = in.levels;
+    const int n = in.n;
+    std::vector<void*> keep;
+    struct Freer {
+        std::vector<void*>* k;
+        ~Freer() {
+            for (void* p : *k) cudaFree(p);
+        }
+    } freer{&keep};
+    auto S = [](int i) { return static_cast<size_t>(i); };
+
+    // ---- first level of every vertex (merge.hpp:106-108), integrality
+    std::vector<int32_t> fl(S(n), 0);
+    for (int i = M - 1; i >= 0; --i)
+        for (int v = in.first[i]; v <= in.last[i]; ++v) fl[S(v)] = i;
+    bool integral = true;
+    long double total = 0;
+    for (long long k = 0; k < in.m; ++k) {
+        const double w = in.edges[k].w;
+        if (!(w >= 0) || w != static_cast<double>(static_cast<int64_t>(w))) integral = false;
+        total += w;
+    }
+    if (total > 4.0e18L) integral = false;
+    for (int i = 0; i < M; ++i)
+        if (in.widths[i] > 32) internal_error("piece wider than 32 vertices in merge");
+
+    std::vector<int32_t> bits_off(S(M));
+    for (int i = 0, off = 0; i < M; ++i) {
+        bits_off[S(i)] = off;
+        off += in.counts[i];
+    }
+    const size_t total_entries = static_cast<size_t>(bits_off[S(M - 1)] + in.counts[M - 1]);
+    std::vector<uint32_t> hbits(in.bits, in.bits + total_entries);
+    std::vector<int32_t> win_start(S(M));
+    for (const Window& W : windows)
+        for (int i = W.s; i < W.e; ++i) win_start[S(i)] = W.s;
+
+    // ---- lex-sorted candidate lists per level: parity 0, parity 1, all
+    std::vector<int32_t> lists;
+    std::vector<WinLevel> wl(S(M));
+    for (int i = 0; i < M; ++i) {
+        WinLevel& L = wl[S(i)];
+        std::memset(&L, 0, sizeof L);
+        L.count = in.counts[i];
+        L.bits_off = bits_off[S(i)];
+        L.first = in.first[i];
+        L.width = in.widths[i];
+        std::vector<int32_t> idx(S(L.count));
+        std::iota(idx.begin(), idx.end(), 0);
+        const uint32_t* b = in.bits + L.bits_off;
+        std::sort(idx.begin(), idx.end(), [&](int a, int c) { return brev_w(b[a]) < brev_w(b[c]); });
+        for (int sel = 0; sel < 3; ++sel) {
+            L.list_off[sel] = static_cast<int32_t>(lists.size());
+            int len = 0;
+            for (int e : idx)
+                if (sel == 2 || static_cast<int>(b[e] & 1u) == sel) {
+                    lists.push_back(e);
+                    ++len;
+                }
+            L.list_len[sel] = len;
+        }
+    }
+    // subtree leaf counts per window (saturating)
+    for (const Window& W : windows) {
+        uint64_t next[2] = {1, 1};
+        for (int i = W.e - 1; i >= W.s; --i) {
+            WinLevel& L = wl[S(i)];
+            uint64_t ns[2] = {0, 0};
+            for (int par = 0; par < 2; ++par)
+                for (int r = 0; r < L.list_len[par]; ++r) {
+                    const uint32_t b = in.bits[L.bits_off + lists[S(L.list_off[par] + r)]];
+                    const int out = static_cast<int>((b >> (L.width - 1)) & 1u);
+                    const unsigned __int128 v = static_cast<unsigned __int128>(ns[par]) + next[out];
+                    ns[par] = v > ~uint64_t{0} ? ~uint64_t{0} : static_cast<uint64_t>(v);
+                }
+            L.nsub[0] = ns[0];
+            L.nsub[1] = ns[1];
+            next[0] = ns[0];
+            next[1] = ns[1];
+        }
+    }
+    int64_t utab_size = 0;
+    for (int i = 0; i < M; ++i) {
+        wl[S(i)].u_off = static_cast<int32_t>(utab_size);
+        utab_size += in.counts[i];
+    }
+
+    // ---- scoring data
+    std::vector<int32_t> pair_off;
+    std::vector<FixedEdge> fixed_edges;
+    std::vector<XEdge> xedges, all_edges;
+    int64_t* d_intra = nullptr;
+    int64_t* d_ptab = nullptr;
+    int64_t* d_utab = nullptr;
+    if (integral) {
+        // groups: (hi level, lo level in the same window); edges to earlier windows are
+        // "fixed" edges of their hi level, folded into the unary table per window.
+        std::vector<std::vector<int32_t>> gid(S(M));
+        for (int i = 0; i < M; ++i) gid[S(i)].assign(S(i - win_start[S(i)] + 1), -1);
+        std::vector<PairGroup> groups;
+        std::vector<std::vector<PairEdge>> pedges;
+        std::vector<std::vector<FixedEdge>> fixed_by_level(S(M));
+        auto group_of = [&](int hi, int lo) -> int32_t {
+            int32_t& g = gid[S(hi)][S(lo - win_start[S(hi)])];
+            if (g < 0) {
+                g = static_cast<int32_t>(groups.size());
+                groups.push_back({hi, lo, 0, 0, 0});
+                pedges.emplace_back();
+            }
+            return g;
+        };
+        for (int i = 0; i < M; ++i) group_of(i, i);  // every level has an intra table
+        for (long long k = 0; k < in.m; ++k) {
+            const qc_edge_t& e = in.edges[k];
+            int lo = fl[S(e.u)], hi = fl[S(e.v)];
+            uint32_t vh = e.v, vl = e.u;
+            if (lo > hi) {
+                std::swap(lo, hi);
+                std::swap(vh, vl);
+            }
+            const int64_t w = static_cast<int64_t>(e.w);
+            if (lo < win_start[S(hi)]) {
+                fixed_by_level[S(hi)].push_back(
+                    {static_cast<int32_t>(vh) - in.first[hi], static_cast<int32_t>(vl), w});
+            } else {
+                pedges[S(group_of(hi, lo))].push_back(
+                    {static_cast<int32_t>(vh) - in.first[hi], static_cast<int32_t>(vl) - in.first[lo], w});
+            }
+        }
+        std::vector<PairEdge> flat;
+        std::vector<PairGroup> gi, gp;
+        int64_t ptab_size = 0;
+        for (size_t g = 0; g < groups.size(); ++g) {
+            PairGroup& G = groups[g];
+            G.e_off = static_cast<int32_t>(flat.size());
+            G.e_len = static_cast<int32_t>(pedges[g].size());
+            flat.insert(flat.end(), pedges[g].begin(), pedges[g].end());
+            if (G.hi == G.lo) {
+                G.out_off = wl[S(G.hi)].u_off;
+                gi.push_back(G);
+            } else {
+                G.out_off = static_cast<int32_t>(ptab_size);
+                ptab_size += static_cast<int64_t>(in.counts[G.hi]) * in.counts[G.lo];
+                gp.push_back(G);
+            }
+        }
+        for (int i = 0; i < M; ++i) {
+            WinLevel& L = wl[S(i)];
+            L.pair_base = static_cast<int32_t>(pair_off.size());
+            for (int j = win_start[S(i)]; j < i; ++j) {
+                const int32_t g = gid[S(i)][S(j - win_start[S(i)])];
+                pair_off.push_back(g < 0 ? -1 : groups[S(g)].out_off);
+            }
+            L.fixed_off = static_cast<int32_t>(fixed_edges.size());
+            L.fixed_len = static_cast<int32_t>(fixed_by_level[S(i)].size());
+            fixed_edges.insert(fixed_edges.end(), fixed_by_level[S(i)].begin(),
+                               fixed_by_level[S(i)].end());
+        }
+        std::vector<int32_t> counts_v(in.counts, in.counts + M);
+        auto* d_pe = dupload(keep, flat, st);
+        auto* d_bits0 = dupload(keep, hbits, st);
+        auto* d_boff = dupload(keep, bits_off, st);
+        auto* d_counts = dupload(keep, counts_v, st);
+        d_intra = dalloc<int64_t>(keep, S(static_cast<int>(utab_size)));
+        d_utab = dalloc<int64_t>(keep, S(static_cast<int>(utab_size)));
+        d_ptab = dalloc<int64_t>(keep, static_cast<size_t>(ptab_size));
+        if (!gi.empty()) {
+            auto* d_gi = dupload(keep, gi, st);
+            k_pair_tables<<<static_cast<unsigned>(gi.size()), 128, 0, st>>>(d_gi, d_pe, d_bits0, d_boff,
+                                                                           d_counts, d_intra);
+            ++*launches;
+        }
+        if (!gp.empty()) {
+            auto* d_gp = dupload(keep, gp, st);
+            k_pair_tables<<<static_cast<unsigned>(gp.size()), 128, 0, st>>>(d_gp, d_pe, d_bits0, d_boff,
+                                                                           d_counts, d_ptab);
+            ++*launches;
+        }
+        QC_CUDA(cudaGetLastError());
+    } else {
+        std::vector<std::vector<XEdge>> buckets(S(M));
+        for (long long k = 0; k < in.m; ++k) {
+            const qc_edge_t& e = in.edges[k];
+            XEdge x{e.u, e.v, e.w, fl[S(e.u)], fl[S(e.v)]};
+            all_edges.push_back(x);
+            buckets[S(std::max(fl[S(e.u)], fl[S(e.v)]))].push_back(x);
+        }
+        for (int i = 0; i < M; ++i) {
+            wl[S(i)].bucket_off = static_cast<int32_t>(xedges.size());
+            wl[S(i)].bucket_len = static_cast<int32_t>(buckets[S(i)].size());
+            xedges.insert(xedges.end(), buckets[S(i)].begin(), buckets[S(i)].end());
+        }
+    }
+
+    // ---- upload common data
+    std::vector<int32_t> first_v(in.first, in.first + M);
+    auto* d_wl = dupload(keep, wl, st);
+    auto* d_lists = dupload(keep, lists, st);
+    auto* d_bits = dupload(keep, hbits, st);
+    auto* d_pair_off = dupload(keep, pair_off, st);
+    auto* d_fixed_edges = dupload(keep, fixed_edges, st);
+    auto* d_xedges = dupload(keep, xedges, st);
+    auto* d_all = dupload(keep, all_edges, st);
+    auto* d_first = dupload(keep, first_v, st);
+    auto* d_asg = dalloc<uint8_t>(keep, S(n));
+    auto* d_acc = dalloc<double>(keep, 1);
+    auto* d_iacc = dalloc<int64_t>(keep, 1);
+    auto* d_leaves = dalloc<uint64_t>(keep, 1);
+    auto* d_dead = dalloc<int>(keep, 1);
+    QC_CUDA(cudaMemsetAsync(d_asg, 0, S(n), st));
+    QC_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(double), st));
+    QC_CUDA(cudaMemsetAsync(d_iacc, 0, sizeof(int64_t), st));
+    QC_CUDA(cudaMemsetAsync(d_leaves, 0, sizeof(uint64_t), st));
+    QC_CUDA(cudaMemsetAsync(d_dead, 0, sizeof(int), st));
+
+    // per-window launch geometry (host upper bound on the leaf count)
+    struct Geo {
+        uint64_t bound;
+        int per_thread;
+        unsigned blocks;
+    };
+    std::vector<Geo> geo;
+    unsigned max_blocks = 1;
+    for (const Window& W : windows) {
+        if (W.e - W.s > kMaxL)
+            resource_error("merge window spans " + std::to_string(W.e - W.s) + " levels (max " +
+                           std::to_string(kMaxL) + ")");
+        const WinLevel& L0 = wl[S(W.s)];
+        auto total_for = [&](int sel) {
+            uint64_t T = 0;
+            for (int r = 0; r < L0.list_len[sel]; ++r) {
+                const uint32_t b = in.bits[L0.bits_off + lists[S(L0.list_off[sel] + r)]];
+                const int out = static_cast<int>((b >> (L0.width - 1)) & 1u);
+                T += (W.e - W.s > 1) ? wl[S(W.s + 1)].nsub[out] : 1;
+            }
+            return T;
+        };
+        uint64_t bound = W.need == 2 ? total_for(2)
+                         : W.need == 3 ? total_for(0)
+                                       : std::max(total_for(0), total_for(1));
+        const uint64_t target_threads = 148ull * 1024;
+        uint64_t per = (bound + target_threads - 1) / target_threads;
+        if (per < 1) per = 1;
+        if (per > (1u << 20)) per = 1u << 20;
+        const uint64_t threads = (bound + per - 1) / per;
+        const uint64_t blocks64 = (threads + kSearchThreads - 1) / kSearchThreads;
+        if (blocks64 > 0x7fffffffull) resource_error("merge enumeration too large");
+        const unsigned blocks = static_cast<unsigned>(std::max<uint64_t>(blocks64, 1));
+        geo.push_back({bound, static_cast<int>(per), blocks});
+        max_blocks = std::max(max_blocks, blocks);
+    }
+    auto* d_bidx = dalloc<uint64_t>(keep, max_blocks);
+    auto* d_bval = dalloc<double>(keep, max_blocks);
+    auto* d_bival = dalloc<int64_t>(keep, max_blocks);
+
+    for (size_t w = 0; w < windows.size(); ++w) {
+        const Window& W = windows[w];
+        SearchArgs A{};
+        A.lv = d_wl + W.s;
+        A.bits = d_bits;
+        A.lists = d_lists;
+        A.utab = d_utab;
+        A.ptab = d_ptab;
+        A.pair_off = d_pair_off;
+        A.xedges = d_xedges;
+        A.all_edges = d_all;
+        A.m_all = static_cast<int32_t>(all_edges.size());
+        A.fixed = d_asg;
+        A.first_of_level = d_first;
+        A.s = W.s;
+        A.L = W.e - W.s;
+        A.need_mode = W.need;
+        A.integral = integral ? 1 : 0;
+        A.full_graph = full_graph ? 1 : 0;
+        A.leaves_per_thread = geo[w].per_thread;
+        A.base_acc = d_acc;
+        A.base_iacc = d_iacc;
+        A.blk_idx = d_bidx;
+        A.blk_val = d_bval;
+        A.blk_ival = d_bival;
+        if (integral) {
+            k_unary<<<static_cast<unsigned>(A.L), 128, 0, st>>>(A, d_intra, d_fixed_edges, d_utab);
+            k_search<true><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
+        } else {
+            k_search<false><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
+        }
+        k_commit<<<1, 1, 0, st>>>(A, static_cast<int>(geo[w].blocks), d_leaves, d_dead, d_acc, d_iacc);
+        *launches += integral ? 3 : 2;
+        QC_CUDA(cudaGetLastError());
+    }
+
+    MergeOutput out;
+    out.assignment.resize(S(n));
+    int dead = 0;
+    QC_CUDA(cudaMemcpyAsync(out.assignment.data(), d_asg, S(n), cudaMemcpyDeviceToHost, st));
+    QC_CUDA(cudaMemcpyAsync(&out.leaves, d_leaves, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    QC_CUDA(cudaMemcpyAsync(&dead, d_dead, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (integral && in.m > 0) {
+        // cut_value re-score on the device (exact for integral weights)
+        std::vector<uint32_t> eu(S(static_cast<int>(in.m))), ev(eu.size());
+        std::vector<double> ew(eu.size());
+        for (long long k = 0; k < in.m; ++k) {
+            eu[S(static_cast<int>(k))] = in.edges[k].u;
+            ev[S(static_cast<int>(k))] = in.edges[k].v;
+            ew[S(static_cast<int>(k))] = in.edges[k].w;
+        }
+        auto* d_eu = dupload(keep, eu, st);
+        auto* d_ev = dupload(keep, ev, st);
+        auto* d_ew = dupload(keep, ew, st);
+        auto* d_cut = dalloc<unsigned long long>(keep, 1);
+        QC_CUDA(cudaMemsetAsync(d_cut, 0, sizeof(unsigned long long), st));
+        const long long blocks = std::min<long long>((in.m + 255) / 256, 148 * 8);
+        k_cut_int<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d_eu, d_ev, d_ew, in.m, d_asg, d_cut);
+        ++*launches;
+        unsigned long long cut = 0;
+        QC_CUDA(cudaMemcpyAsync(&cut, d_cut, sizeof cut, cudaMemcpyDeviceToHost, st));
+        QC_CUDA(cudaStreamSynchronize(st));
+        out.value = static_cast<double>(cut);
+    } else {
+        QC_CUDA(cudaStreamSynchronize(st));
+        double v = 0.0;  // graph.hpp:126-134, edge-list order
+        for (long long k = 0; k < in.m; ++k)
+            if (out.assignment[in.edges[k].u] != out.assignment[in.edges[k].v]) v += in.edges[k].w;
+        out.value = v;
+    }
+    if (dead) config_error("no compatible candidate chain exists");
+    return out;
+}
+
+}  // namespace qcg

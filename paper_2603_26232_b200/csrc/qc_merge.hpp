@@ -1,0 +1,48 @@
+// Host-facing merge declarations (qc_merge.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace qcg {
+
+struct qc_edge_t {  // == qc_edge (qcgpu.h) == qcut::Edge layout
+    uint32_t u, v;
+    double w;
+};
+
+struct MergeInput {
+    int n = 0;                       // vertices
+    long long m = 0;                 // edges
+    const qc_edge_t* edges = nullptr;
+    int levels = 0;                  // pool levels
+    const int32_t* widths = nullptr;
+    const int32_t* counts = nullptr;
+    const uint32_t* bits = nullptr;  // concatenated, pool order
+    int pieces = 0;                  // chain pieces
+    const int32_t* first = nullptr;
+    const int32_t* last = nullptr;
+};
+
+// One exhaustive search over levels [s, e). need: 2 free, 3 halve (bit 0 clear),
+// -1 = seam bit read from the assignment committed by the previous window.
+struct Window {
+    int s, e, need;
+};
+
+struct MergeOutput {
+    double value = 0.0;              // cut_value of the best assignment (re-scored)
+    std::vector<uint8_t> assignment; // n bytes
+    uint64_t leaves = 0;
+};
+
+void check_pool(const MergeInput& in);
+double estimate_paths(const int32_t* counts, int M, bool halve);
+// Runs the windows back to back on `st` and returns the re-scored result.
+// full_graph selects MergeEval::kFullGraph scoring (merge.hpp:164) on the exact path.
+MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
+                      cudaStream_t st, uint64_t* launches);
+
+}  // namespace qcg

@@ -1,0 +1,130 @@
+"""GPU parity: statevector.hpp / qaoa.hpp hot path through the C-ABI vs the oracle.
+
+Bit-exact (==) on the integral-weight path: amplitudes, expectation, probabilities,
+top-K bits; mirrors test_statevector.cpp / test_qaoa.cpp and acceptance crit 6.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_state(q, seed):
+    rng = np.random.default_rng(seed)
+    v = rng.normal(size=(1 << q)) + 1j * rng.normal(size=(1 << q))
+    return (v / np.sqrt(np.sum(np.abs(v) ** 2))).astype(np.complex128)
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64)) or \
+        np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("q,p_edge,seed", [(2, 1.0, 0), (5, 0.5, 3), (10, 0.3, 1), (13, 0.3, 2),
+                                           (14, 0.3, 4), (16, 0.2, 5), (20, 0.1, 6)])
+@pytest.mark.parametrize("layers", [1, 2, 3])
+def test_run_ansatz_bit_exact(engine, oracle, q, p_edge, seed, layers):
+    e = oracle.generate_er(q, p_edge, seed)
+    rng = np.random.default_rng(seed + 100 * layers)
+    g = rng.uniform(0, np.pi, layers)
+    b = rng.uniform(0, np.pi, layers)
+    a_ref, ex_ref = oracle.run_ansatz(q, e, g, b)
+    a_gpu, ex_gpu = engine.run_ansatz(q, e, g, b)
+    assert np.array_equal(a_gpu, a_ref)
+    assert ex_gpu == ex_ref
+
+
+def test_ramp_skips_are_exact(engine, oracle):
+    # p=1 ramp: beta = 0 (mixer skipped); gamma = 0 (phase skipped)
+    e = oracle.generate_er(12, 0.4, 9)
+    for g, b in [([np.pi / 2], [0.0]), ([0.0], [0.7]), ([0.0], [0.0])]:
+        a_ref, ex_ref = oracle.run_ansatz(12, e, g, b)
+        a_gpu, ex_gpu = engine.run_ansatz(12, e, g, b)
+        assert np.array_equal(a_gpu, a_ref)
+        assert ex_gpu == ex_ref
+
+
+@pytest.mark.parametrize("q", [1, 3, 8, 12, 13, 15])
+def test_layers_on_arbitrary_states(engine, oracle, q):
+    e = oracle.generate_er(q, 0.5, q) if q > 1 else np.zeros(0, oracle_edge_dtype())
+    s = rand_state(q, 11 + q)
+    assert np.array_equal(engine.apply_mixer_layer(s, 0.77), oracle.apply_mixer_layer(s, 0.77))
+    assert np.array_equal(engine.apply_cost_layer(s, q, e, 1.3),
+                          oracle.apply_cost_layer(s, q, e, 1.3))
+    assert engine.expectation(s, q, e) == oracle.expectation(s, q, e)
+    assert engine.norm_sq(s) == oracle.norm_sq(s)
+
+
+def oracle_edge_dtype():
+    from oracle.refpy import EDGE_DTYPE
+    return EDGE_DTYPE
+
+
+def test_identities(engine):
+    e = [(0, 1), (1, 2), (0, 2)]
+    s = rand_state(3, 1)
+    assert np.array_equal(engine.apply_cost_layer(s, 3, e, 0.0), s)  # statevector.hpp:149
+    assert np.array_equal(engine.apply_mixer_layer(s, 0.0), s)       # statevector.hpp:193
+    one = engine.apply_mixer_layer(np.array([1, 0], np.complex128), np.pi / 2)
+    assert abs(one[0]) < 1e-12 and abs(one[1] - (-1j)) < 1e-12      # test_statevector.cpp:137
+    plus = engine.plus_state(2)
+    out = engine.apply_cost_layer(plus, 2, [(0, 1)], np.pi)          # test_statevector.cpp:95
+    assert np.allclose(out.real, [0.5, -0.5, -0.5, 0.5], atol=1e-12)
+
+
+def test_plus_state(engine, oracle):
+    for q in (1, 3, 12, 14):
+        assert np.array_equal(engine.plus_state(q, 24), oracle.plus_state(q, 24))
+
+
+@pytest.mark.parametrize("q,k,fold", [(2, 2, True), (2, 4, False), (5, 16, True), (9, 4, True),
+                                      (12, 7, False), (14, 8, True), (16, 1500, True)])
+def test_top_candidates_random(engine, oracle, q, k, fold):
+    s = rand_state(q, q * 7 + k)
+    b0, p0 = oracle.top_candidates(s, k, fold)
+    b1, p1 = engine.top_candidates(s, k, fold)
+    assert np.array_equal(b1, b0)
+    assert np.array_equal(p1, p0)
+
+
+def test_top_candidates_tie_order(engine):
+    # test_qaoa.cpp:116-139: folded classes and lexicographic tie order 0,3,2,1
+    s = np.sqrt(np.array([0.4, 0.1, 0.1, 0.4])).astype(np.complex128)
+    b, p = engine.top_candidates(s, 2, True)
+    assert list(b) == [0, 2] and abs(p[0] - 0.8) < 1e-12 and abs(p[1] - 0.2) < 1e-12
+    b, _ = engine.top_candidates(s, 4, False)
+    assert list(b) == [0, 3, 2, 1]
+
+
+def test_top_candidates_plateaus(engine, oracle):
+    # QAOA states of sparse graphs have huge plateaus of exactly equal probabilities
+    e = oracle.generate_er(10, 0.1, 0)
+    a, _ = oracle.run_ansatz(10, e, [1.1], [0.4])
+    for k in (1, 4, 37, 512):
+        b0, p0 = oracle.top_candidates(a, k, True)
+        b1, p1 = engine.top_candidates(a, k, True)
+        assert np.array_equal(b1, b0) and np.array_equal(p1, p0)
+
+
+def test_eval_batch_matches_oracle(engine, oracle):
+    graphs = [(q, oracle.generate_er(q, 0.3, q)) for q in (4, 9, 14, 15)]
+    rng = np.random.default_rng(5)
+    idx = np.array([0, 1, 2, 3, 2, 1, 0, 3], np.int32)
+    params = rng.uniform(0, np.pi, (len(idx), 4))
+    out = engine.eval_batch(graphs, 2, idx, params)
+    for k, i in enumerate(idx):
+        n, e = graphs[i]
+        _, ex = oracle.run_ansatz(n, e, params[k, :2], params[k, 2:], want_amps=False)
+        assert out[k] == ex
+
+
+def test_errors_map_to_reference_types(engine):
+    from paper_2603_26232_b200 import ConfigError, ResourceError
+    with pytest.raises(ConfigError):
+        engine.top_candidates(rand_state(3, 0), 5, True)  # > 4 folded classes
+    with pytest.raises(ConfigError):
+        engine.solve_subgraph(0, [])
+    with pytest.raises(ResourceError):
+        engine.solve_subgraph(21, [(0, 20)])  # default cap 20 (test_qaoa.cpp:243-254)
+    with pytest.raises(ConfigError):
+        engine.run_ansatz(3, [(0, 0)], [0.1], [0.1])  # self-loop
