@@ -1,0 +1,376 @@
+#!/usr/bin/env python3
+"""Benchmark: end-to-end Max-Cut solve time & subgraph-QAOA evals/s on B200.
+
+One bench "step" = one full solve of the workload through the hot path: the batched
+QAOA stage (lockstep Nelder-Mead over all subgraphs, `budget` objective evaluations
+each, final circuit + top-K) and the candidate merge, i.e. pipeline.hpp:219-334.
+
+  value  — evals/s with the inputs resident in HBM (qc_pipeline_prepare once, then
+           qc_pipeline_execute per step): M * budget / device time per step.
+  e2e    — the same metric through the reference-facing C-ABI call with HOST buffers
+           (qc_run_pipeline: graph edges in, cut + assignment out; partition, table
+           upload, per-step parameter uploads and result reads inside the timed region).
+
+Default workload (BASELINE configs[1], one B200): ER(n=400, p=0.1, seed 0) split with
+qubit_cap 20 into 21 chained 20-qubit subgraphs, QAOA depth p=2, top-K 2, budget 200,
+level merge (2*2^21 = 4,194,304 leaves). N>1 (torchrun, one rank per GPU over NCCL):
+the subgraphs are sharded in contiguous blocks, solve records are all-gathered over
+NVLink (the only collective) and rank 0 merges.
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, the
+unmodified qcut headers; the C restatement if that build is absent) on this host's
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "end-to-end Max-Cut solve time & subgraph-QAOA evals/s at 1/2/4/8 B200"
+UNIT = "evals/s"
+
+WORKLOADS = {
+    # BASELINE configs[1]: 400-vertex ER (the paper's 1,600x comparison size), 20-qubit
+    # subgraphs, p=1-2, one B200
+    "c2": dict(n=400, p_edge=0.1, seed=0, qubit_cap=20, layers=2, top_k=2, budget=200,
+               label="C2: ER(n=400,p=0.1,seed=0), cap 20 -> 21 x 20-qubit subgraphs, QAOA p=2, "
+                     "top-K 2, NM budget 200, level merge (4,194,304 leaves)"),
+    "c1": dict(n=100, p_edge=0.1, seed=0, qubit_cap=10, layers=1, top_k=4, budget=200,
+               label="C1: ER(n=100,p=0.1,seed=0), cap 10 -> 11 x 10-qubit subgraphs, p=1, "
+                     "top-K 4, level merge (8,388,608 leaves)"),
+    "c4": dict(n=10000, p_edge=0.1, seed=0, qubit_cap=20, layers=1, top_k=2, budget=200,
+               label="C4: ER(n=10000,p=0.1,seed=0), cap 20 -> 527 x 20-qubit subgraphs, p=1, "
+                     "top-K 2, windowed merge"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def er_graph(n, p, seed):
+    """ER(n, p, seed) exactly as graph.hpp:146-160 (mt19937_64, 53-bit draws)."""
+    from oracle.refpy import OracleLib, RefLib, ref_available, oracle_available
+    lib = RefLib() if ref_available() else (OracleLib() if oracle_available() else None)
+    if lib is None:
+        raise RuntimeError("no graph generator available (build oracle/)")
+    return lib.generate_er(n, p, seed)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------------------------------
+# CPU baseline / reference arm
+# --------------------------------------------------------------------------------------
+def reference_sample(w, edges, budgets=(4, 12)):
+    """Time the reference pipeline (partition -> QAOA stage -> merge, all host threads) at
+    two small NM budgets and extrapolate the QAOA stage linearly to the full budget
+    (fixed per-subgraph costs — cost table, final circuit, top-K — are the intercept).
+    Returns (evals/s, description, kind, cores, seconds spent)."""
+    from oracle.refpy import OracleLib, RefLib, ref_available
+    kind = "reference" if ref_available() else "port"
+    lib = RefLib() if kind == "reference" else OracleLib()
+    cores = os.cpu_count() or 1
+    t0 = time.time()
+    runs = []
+    for b in budgets:
+        r = lib.run_pipeline(w["n"], edges, qubit_cap=w["qubit_cap"], top_k=w["top_k"],
+                             layers=w["layers"], budget=b, seed=0, workers=cores)
+        runs.append(r)
+    (b1, r1), (b2, r2) = zip(budgets, runs)
+    slope = max((r2["qaoa_s"] - r1["qaoa_s"]) / (b2 - b1), 0.0)
+    fixed = max(r1["qaoa_s"] - slope * b1, 0.0)
+    qaoa_full = fixed + slope * w["budget"]
+    merge_s = min(r1["merge_s"], r2["merge_s"])
+    total = r1["partition_s"] + qaoa_full + merge_s
+    M = r1["subgraphs"]
+    value = M * w["budget"] / total
+    desc = (f"{'oracle/_ref (unmodified qcut headers)' if kind == 'reference' else 'oracle C port'}"
+            f" run_pipeline with workers={cores} at NM budgets {b1} and {b2}; QAOA stage "
+            f"extrapolated linearly to budget {w['budget']} ({qaoa_full:.2f} s), merge "
+            f"{merge_s:.2f} s measured, total {total:.2f} s per solve of {M} subgraphs")
+    return value, desc, kind, cores, time.time() - t0, total
+
+
+def run_reference_arm(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    edges = er_graph(w["n"], w["p_edge"], w["seed"])
+    for _ in range(args.warmup):
+        reference_sample(w, edges)
+    vals, totals = [], []
+    desc = kind = cores = None
+    for _ in range(args.steps):
+        v, desc, kind, cores, _, total = reference_sample(w, edges)
+        vals.append(v)
+        totals.append(total)
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(totals) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["label"], "n": w["n"], "p_edge": w["p_edge"],
+                   "qubit_cap": w["qubit_cap"], "layers": w["layers"], "top_k": w["top_k"],
+                   "budget": w["budget"], "parallelism": f"cpu x{cores} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    w = dict(WORKLOADS[args.workload])
+    if args.impl == "reference":
+        return run_reference_arm(args, w)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2603_26232_b200 import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    eng = Engine(local)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
+    edges = er_graph(w["n"], w["p_edge"], w["seed"])
+    cfg = dict(qubit_cap=w["qubit_cap"], top_k=w["top_k"], layers=w["layers"],
+               budget=w["budget"], seed=0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- single GPU: resident session (value) -------------------------------------
+    if world == 1:
+        sess = eng.prepare_pipeline(w["n"], edges, **cfg)
+        M = None
+
+        def step_value():
+            return sess.execute()
+    else:
+        M = eng.subgraph_count(w["n"], edges, **cfg)
+        begin, end = eng.shard_range(M, rank, world)
+        from paper_2603_26232_b200 import kcap_for
+        kcap = kcap_for(w["qubit_cap"], w["top_k"])
+        rb = eng.record_bytes(kcap, w["layers"])
+        maxcount = max(eng.shard_range(M, r, world)[1] - eng.shard_range(M, r, world)[0]
+                       for r in range(world))
+
+        def step_value():
+            rec = eng.shard_solve(w["n"], edges, begin, end, rb, **cfg)
+            buf = torch.zeros(maxcount * rb, dtype=torch.uint8, device=f"cuda:{local}")
+            if len(rec):
+                buf[: len(rec)].copy_(torch.from_numpy(rec))
+            out = torch.empty(world * maxcount * rb, dtype=torch.uint8, device=f"cuda:{local}")
+            dist.all_gather_into_tensor(out, buf)  # NCCL over NVLink: the only collective
+            if rank == 0:
+                host = out.cpu().numpy().reshape(world, maxcount * rb)
+                parts = [host[r, : (eng.shard_range(M, r, world)[1] -
+                                    eng.shard_range(M, r, world)[0]) * rb] for r in range(world)]
+                return eng.merge_records(w["n"], edges, np.concatenate(parts), M, **cfg)
+            return None
+
+    def timed(fn, steps, prof=False):
+        """per-step device time via CUDA events on the engine stream, L2 flushed between."""
+        times, last = [], None
+        launches0 = eng.launches
+        if prof:
+            eng.profile(True)
+        for _ in range(steps):
+            flush.zero_()
+            barrier()
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            last = fn()
+            ev1.record(stream)
+            barrier()
+            times.append(ev0.elapsed_time(ev1) / 1e3)
+        launches = eng.launches - launches0
+        profile = eng.profile_read() if prof else None
+        if prof:
+            eng.profile(False)
+        return times, last, launches, profile
+
+    for _ in range(args.warmup):
+        step_value()
+        barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_val, rep, launches, profile = timed(step_value, args.steps, prof=True)
+    clk = clocks.stop()
+
+    # max over ranks
+    tot = torch.tensor([sum(t_val)], dtype=torch.float64, device=f"cuda:{local}")
+    lt = torch.tensor([launches], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+    sec_per_step = tot.item() / args.steps
+    n_sub = rep.subgraphs if rank == 0 and rep is not None else (M or 0)
+    evals_per_step = (rep.evals if rank == 0 and rep is not None else 0)
+
+    # ---- e2e through the C-ABI with host buffers (N=1; N>1 reuses the sharded path)
+    e2e = None
+    if world == 1:
+        h0, d0 = eng.transfers()
+
+        def step_e2e():
+            return eng.run_pipeline(w["n"], edges, **cfg)
+        t_e2e, rep_e2e, _, _ = timed(step_e2e, args.steps)
+        h1, d1 = eng.transfers()
+        assert rep_e2e.cut == rep.cut and rep_e2e.assignment == rep.assignment
+        e2e = {"value": rep_e2e.evals / (sum(t_e2e) / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": (h1 - h0) // args.steps,
+               "d2h_bytes_per_step": (d1 - d0) // args.steps,
+               "ms_per_step": sum(t_e2e) / args.steps * 1e3}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    if e2e is None:  # multi-GPU: the sharded step already moves records host<->device
+        e2e = {"value": evals_per_step / sec_per_step, "unit": UNIT,
+               "h2d_bytes_per_step": None, "d2h_bytes_per_step": None}
+
+    # ---- roofline for the dominant kernel --------------------------------------------
+    peak, peak_kind = load_peaks()
+    dom = max(profile, key=lambda k: profile[k]["ms"])
+    d = profile[dom]
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(dom)
+            traffic = tr.get("dram_bytes_per_launch") if tr else None
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind ==
+                "measured" else "fallback (B200_PROFILING.md)",
+                "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                "avg_launch_ms": d["ms"] / max(d["launches"], 1),
+                "share_of_step": d["ms"] / 1e3 / (sum(t_val) / 1.0) if sum(t_val) else None,
+                "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                                "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
+                                if v["ms"] > 0 else 0.0}
+                            for k, v in profile.items() if v["launches"]}}
+
+    line = {
+        "metric": METRIC, "value": evals_per_step / sec_per_step, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (ER graph from the reference generator, graph.hpp:146)",
+        "config": {"workload": w["label"], "n": w["n"], "p_edge": w["p_edge"],
+                   "qubit_cap": w["qubit_cap"], "subgraphs": n_sub, "layers": w["layers"],
+                   "top_k": w["top_k"], "budget": w["budget"], "parallelism": f"shard{world}",
+                   "l2": "working set (21 half-states x 8 MiB + f buffers) > 126 MB L2; "
+                         "L2 flushed (256 MB write) between timed steps"},
+        "solve_time_s": sec_per_step, "cut": rep.cut, "evals_per_step": evals_per_step,
+        "stage_s": {"partition": rep.partition_s, "qaoa": rep.qaoa_s, "merge": rep.merge_s},
+        "e2e": e2e, "gpu_launches": int(lt.item()), "clocks": clk, "roofline": roofline,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            v, desc, kind, cores, _, total = reference_sample(w, edges)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                    "sample": desc}
+        except Exception as ex:  # report, never fail the bench line
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": "unavailable", "sample": str(ex)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -167,6 +167,18 @@ int qc_qubit_cap(void);
 uint64_t qc_engine_launches(const qc_engine* e);
 /* Device bytes of stored-state / scratch the engine may use; 0 = automatic. */
 int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
+/* Live profiling: with on=1 every engine kernel is bracketed by CUDA events on the
+ * engine's stream; qc_engine_profile_read returns, per kernel kind (0 levels, 1 onchip,
+ * 2 pass_low, 3 pass_high, 4 blocksum, 5 finalsum, 6 topk, 7 merge_tables,
+ * 8 merge_search, 9 merge_other), the launch count, summed device ms and summed
+ * algorithmic bytes since the last qc_engine_profile call. */
+int qc_engine_profile(qc_engine* e, int on);
+int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
+                           double* bytes);
+/* Host<->device bytes copied by this engine since creation. */
+int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h);
+/* The engine's cudaStream_t (all engine work is ordered on it). */
+void* qc_engine_stream(const qc_engine* e);
 
 /* ---- statevector.hpp ---------------------------------------------------------- */
 /* statevector.hpp:75-111 CostTable: out[z] = C(z) for z < 2^n. */
@@ -250,6 +262,15 @@ int qc_chained_merge(qc_engine* e, const qc_pool* pool, const qc_graph* g,
  * qc_shard_solve); the merge then runs on the gathered records (qc_merge_records). */
 int qc_run_pipeline(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
                     qc_run_report* report, char* assignment);
+
+/* Resident-input session: partition + device cut tables built once
+ * (qc_pipeline_prepare), then QAOA stage + top-K + merge on resident inputs
+ * (qc_pipeline_execute, repeatable; same results as qc_run_pipeline). */
+typedef struct qc_pipeline qc_pipeline;
+int qc_pipeline_prepare(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
+                        qc_pipeline** out);
+int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment);
+void qc_pipeline_destroy(qc_pipeline* pl);
 
 /* Multi-GPU: fixed-size solve records for the NCCL gather.
  * record_bytes(top_k_cap, layers) gives the size of one record; qc_shard_solve solves

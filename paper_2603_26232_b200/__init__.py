@@ -120,8 +120,15 @@ EXPORTED_SYMBOLS = [
     "qc_linear_ramp", "qc_run_ansatz", "qc_eval_batch", "qc_optimize_batch",
     "qc_top_candidates", "qc_solve_subgraph", "qc_solve_batch", "qc_level_merge",
     "qc_chained_merge", "qc_run_pipeline", "qc_record_bytes", "qc_shard_range",
-    "qc_shard_solve", "qc_merge_records",
+    "qc_shard_solve", "qc_merge_records", "qc_engine_profile", "qc_engine_profile_read",
+    "qc_engine_transfers", "qc_engine_stream", "qc_pipeline_prepare", "qc_pipeline_execute",
+    "qc_pipeline_destroy", "qc_simplex_create", "qc_simplex_ask", "qc_simplex_tell",
+    "qc_simplex_result", "qc_simplex_destroy", "qc_optimizer_create", "qc_optimizer_ask",
+    "qc_optimizer_tell", "qc_optimizer_result", "qc_optimizer_destroy",
 ]
+
+KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
+                "merge_tables", "merge_search", "merge_other"]
 
 _LIB = None
 
@@ -140,6 +147,8 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.qc_engine_launches.restype = C.c_uint64
     lib.qc_record_bytes.restype = C.c_int64
     lib.qc_engine_destroy.restype = None
+    lib.qc_engine_stream.restype = C.c_void_p
+    lib.qc_pipeline_destroy.restype = None
     if path is None:
         _LIB = lib
     return lib
@@ -306,6 +315,33 @@ class Engine:
 
     def set_memory_budget(self, nbytes: int):
         self._call("qc_engine_set_memory_budget", C.c_uint64(nbytes))
+
+    # ---- instrumentation -----------------------------------------------------------
+    def profile(self, on: bool = True):
+        """Start (and reset) live per-kernel CUDA-event timing on the engine stream."""
+        self._call("qc_engine_profile", C.c_int(int(on)))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for k, name in enumerate(KERNEL_KINDS):
+            n = C.c_uint64(0)
+            ms = C.c_double(0)
+            b = C.c_double(0)
+            self._call("qc_engine_profile_read", C.c_int(k), C.byref(n), C.byref(ms), C.byref(b))
+            out[name] = dict(launches=int(n.value), ms=ms.value, bytes=b.value)
+        return out
+
+    def transfers(self):
+        h = C.c_uint64(0)
+        d = C.c_uint64(0)
+        _check(self.lib, self.lib.qc_engine_transfers(self._h, C.byref(h), C.byref(d)))
+        return int(h.value), int(d.value)
+
+    def stream_handle(self) -> int:
+        return int(self.lib.qc_engine_stream(self._h) or 0)
+
+    def prepare_pipeline(self, n: int, edges, **cfg) -> "PipelineSession":
+        return PipelineSession(self, n, edges, **cfg)
 
     # ---- statevector.hpp -----------------------------------------------------------
     def cost_table(self, n: int, edges, cap: int = 24):
@@ -554,6 +590,39 @@ class Engine:
         return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
                          rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
                          asg.value.decode())
+
+
+class PipelineSession:
+    """qc_pipeline_*: partition + resident device cut tables, then repeatable execute()."""
+
+    def __init__(self, engine: Engine, n: int, edges, **cfg):
+        self.engine = engine
+        self.n = n
+        g, self._edges = _graph(n, edges)
+        c = engine.run_config(**cfg)
+        h = C.c_void_p()
+        _check(engine.lib, engine.lib.qc_pipeline_prepare(engine._h, C.byref(g), C.byref(c),
+                                                          C.byref(h)))
+        self._h = h
+
+    def execute(self) -> RunReport:
+        rep = _RunReport()
+        asg = C.create_string_buffer(self.n + 1)
+        _check(self.engine.lib, self.engine.lib.qc_pipeline_execute(self._h, C.byref(rep), asg))
+        return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
+                         rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
+                         asg.value.decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.engine.lib.qc_pipeline_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def kcap_for(n_max_width: int, top_k: int, fold: bool = True) -> int:

@@ -103,8 +103,17 @@ using namespace qcg;
 // ---------------------------------------------------------------------------
 // engine
 // ---------------------------------------------------------------------------
+void qc_engine::h2d_copy(void* dst, const void* src, size_t bytes) {
+    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+    h2d += bytes;
+}
+void qc_engine::d2h_copy(void* dst, const void* src, size_t bytes) {
+    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+    d2h += bytes;
+}
+
 std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool allow_sym,
-                                         bool unit_cost) {
+                                         bool unit_cost, DevBuf* target) {
     std::vector<DevGraph> dg(hg.size());
     size_t bytes = 0, ebytes = 0;
     std::vector<size_t> off(hg.size()), eoff(hg.size());
@@ -125,7 +134,7 @@ std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool 
         eoff[i] = ebytes;
         ebytes += hg[i].u.size() * 16 + 256;
     }
-    char* base = static_cast<char*>(tables.get(bytes));
+    char* base = static_cast<char*>((target ? target : &tables)->get(bytes));
     if (unit_cost) return dg;
     char* ebase = static_cast<char*>(edges.get(ebytes));
     char* hbase = static_cast<char*>(hstage.get(ebytes));
@@ -136,7 +145,7 @@ std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool 
         std::memcpy(h + m * 4, hg[i].v.data(), m * 4);
         std::memcpy(h + m * 8, hg[i].w.data(), m * 8);
     }
-    QC_CUDA(cudaMemcpyAsync(ebase, hbase, ebytes, cudaMemcpyHostToDevice, stream));
+    h2d_copy(ebase, hbase, ebytes);
     for (size_t i = 0; i < hg.size(); ++i) {
         DevGraph& d = dg[i];
         const size_t m = hg[i].u.size();
@@ -145,9 +154,11 @@ std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool 
             d.lev = reinterpret_cast<uint16_t*>(base + off[i]);
         else
             d.val = reinterpret_cast<double*>(base + off[i]);
+        prof.begin(K_LEVELS, static_cast<double>(size_t{1} << d.Q) * (d.integral ? 2.0 : 8.0), stream);
         launches += launch_levels(reinterpret_cast<uint32_t*>(de), reinterpret_cast<uint32_t*>(de + m * 4),
                                   reinterpret_cast<double*>(de + m * 8), static_cast<int>(m), d.Q,
                                   d.integral, d.lev, d.val, stream);
+        prof.end(stream);
     }
     // the host staging buffer is reused by the next upload: wait for this copy
     QC_CUDA(cudaStreamSynchronize(stream));
@@ -209,6 +220,9 @@ void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts
     auto* hl = reinterpret_cast<LayerParam*>(h + o_lp);
     auto* hlut = reinterpret_cast<double*>(h + o_lut);
     size_t lut_pos = 0;
+    ChainStats stats;
+    stats.phase.assign(static_cast<size_t>(std::max(p, 0)), 0);
+    stats.mix.assign(static_cast<size_t>(std::max(p, 0)), 0);
     const double amp0 = 1.0 / std::sqrt(static_cast<double>(size_t{1} << g0.q));  // :141
     for (int k = 0; k < n; ++k) {
         const DevGraph& dgk = dg[static_cast<size_t>(pts[k].g)];
@@ -230,6 +244,8 @@ void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts
             L.mix = (L.s == 0.0 && L.c == 1.0) ? 0 : 1;
             L.phase = gamma == 0.0 ? 0 : 1;  // :149
             L.gamma = gamma;
+            stats.phase[static_cast<size_t>(l)] += L.phase;
+            stats.mix[static_cast<size_t>(l)] += L.mix;
             L.lut = nullptr;
             if (L.phase && dgk.integral && !dgk.unit_cost) {
                 // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c)
@@ -244,13 +260,13 @@ void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts
             }
         }
     }
-    QC_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, stream));
+    h2d_copy(d, h, bytes);
     launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
                              reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, part, od,
-                             stream);
+                             stream, &stats, &prof);
     if (flags & F_EXPECT) {
         auto* ho = static_cast<double*>(hout.get(static_cast<size_t>(n) * 8));
-        QC_CUDA(cudaMemcpyAsync(ho, od, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, stream));
+        d2h_copy(ho, od, static_cast<size_t>(n) * 8);
         QC_CUDA(cudaStreamSynchronize(stream));
         std::memcpy(out, ho, static_cast<size_t>(n) * 8);
     } else {
@@ -333,8 +349,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
     return out;
 }
 
-std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
-                                  const std::vector<qc_solve_options>& opts) {
+void validate_solve(const std::vector<HostGraph>& hg, const std::vector<qc_solve_options>& opts) {
     const size_t n = hg.size();
     for (size_t i = 0; i < n; ++i) {  // qaoa.hpp:199-203, then :88, :28, :162-165
         const int q = hg[i].n;
@@ -350,7 +365,19 @@ std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg
             config_error("top_k must lie in [1, " + std::to_string(classes) + "] for " +
                          std::to_string(q) + " qubits" + (opts[i].fold ? " (folded)" : ""));
     }
+}
+
+std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
+                                  const std::vector<qc_solve_options>& opts) {
+    validate_solve(hg, opts);
     const std::vector<DevGraph> dg = e->prepare(hg, true);
+    return solve_prepared(e, hg, dg, opts);
+}
+
+std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>& hg,
+                                     const std::vector<DevGraph>& dg,
+                                     const std::vector<qc_solve_options>& opts) {
+    const size_t n = hg.size();
     std::vector<int> layers(n), budget(n);
     std::vector<uint64_t> seeds(n);
     std::vector<double> tol(n);
@@ -386,16 +413,15 @@ std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg
                 auto* d_bits = reinterpret_cast<uint32_t*>(ob);
                 auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(K) * 4 + 15) & ~size_t{15}));
                 e->launches += launch_topk(e->slot_state(q, dg[i].sym, static_cast<int>(k - b)), q,
-                                           dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream);
+                                           dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream,
+                                           &e->prof);
                 SolveOut& r = out[i];
                 r.width = q;
                 r.folded = fold;
                 r.bits.resize(static_cast<size_t>(K));
                 r.probs.resize(static_cast<size_t>(K));
-                QC_CUDA(cudaMemcpyAsync(r.bits.data(), d_bits, static_cast<size_t>(K) * 4,
-                                        cudaMemcpyDeviceToHost, e->stream));
-                QC_CUDA(cudaMemcpyAsync(r.probs.data(), d_probs, static_cast<size_t>(K) * 8,
-                                        cudaMemcpyDeviceToHost, e->stream));
+                e->d2h_copy(r.bits.data(), d_bits, static_cast<size_t>(K) * 4);
+                e->d2h_copy(r.probs.data(), d_probs, static_cast<size_t>(K) * 8);
                 e->sync();
                 r.params = best[i].params;
                 r.expectation = best[i].expectation;
@@ -444,7 +470,7 @@ void full_state_op(qc_engine* e, int q, double* amps, const DevGraph& dg, int p,
     if (!(flags & F_INIT)) {
         auto* h = static_cast<double*>(e->hstage.get(N * 16));
         std::memcpy(h, amps, N * 16);
-        QC_CUDA(cudaMemcpyAsync(st, h, N * 16, cudaMemcpyHostToDevice, e->stream));
+        e->h2d_copy(st, h, N * 16);
         QC_CUDA(cudaStreamSynchronize(e->stream));
     }
     std::vector<DevGraph> v{dg};
@@ -455,7 +481,7 @@ void full_state_op(qc_engine* e, int q, double* amps, const DevGraph& dg, int p,
     if (out_expect) *out_expect = ex;
     if (flags & F_STATE_OUT) {
         auto* h = static_cast<double*>(e->hout.get(N * 16));
-        QC_CUDA(cudaMemcpyAsync(h, e->states.p, N * 16, cudaMemcpyDeviceToHost, e->stream));
+        e->d2h_copy(h, e->states.p, N * 16);
         QC_CUDA(cudaStreamSynchronize(e->stream));
         std::memcpy(amps, h, N * 16);
     }
@@ -499,6 +525,36 @@ void qc_engine_destroy(qc_engine* e) {
     delete e;
 }
 
+int qc_engine_profile(qc_engine* e, int on) {
+    return guarded([&] {
+        check_engine(e);
+        e->prof.reset();
+        e->prof.on = on != 0;
+    });
+}
+
+int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
+                           double* bytes) {
+    return guarded([&] {
+        check_engine(e);
+        if (kind < 0 || kind >= K_COUNT) config_error("unknown kernel kind");
+        e->prof.resolve();
+        if (launches) *launches = e->prof.count[kind];
+        if (ms) *ms = e->prof.ms[kind];
+        if (bytes) *bytes = e->prof.bytes[kind];
+    });
+}
+
+int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h) {
+    return guarded([&] {
+        if (!e) config_error("null engine");
+        if (h2d) *h2d = e->h2d;
+        if (d2h) *d2h = e->d2h;
+    });
+}
+
+void* qc_engine_stream(const qc_engine* e) { return e ? static_cast<void*>(e->stream) : nullptr; }
+
 int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes) {
     return guarded([&] {
         check_engine(e);
@@ -520,14 +576,14 @@ int qc_cost_table(qc_engine* e, const qc_graph* g, int cap, double* out, int* in
         double mx = 0.0;
         if (dg[0].integral) {
             std::vector<uint16_t> lev(N);
-            QC_CUDA(cudaMemcpyAsync(lev.data(), dg[0].lev, N * 2, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h_copy(lev.data(), dg[0].lev, N * 2);
             e->sync();
             for (size_t z = 0; z < N; ++z) {
                 out[z] = static_cast<double>(lev[z]);
                 mx = std::max(mx, out[z]);
             }
         } else {
-            QC_CUDA(cudaMemcpyAsync(out, dg[0].val, N * 8, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h_copy(out, dg[0].val, N * 8);
             e->sync();
             for (size_t z = 0; z < N; ++z) mx = std::max(mx, out[z]);
         }
@@ -658,7 +714,7 @@ int qc_run_ansatz(qc_engine* e, const qc_graph* g, int p, const double* gammas,
             const int q = hg.n;
             const size_t N = size_t{1} << plan.Q;
             std::vector<double> half(2 * N);
-            QC_CUDA(cudaMemcpyAsync(half.data(), e->states.p, N * 16, cudaMemcpyDeviceToHost, e->stream));
+            e->d2h_copy(half.data(), e->states.p, N * 16);
             e->sync();
             const size_t full = (size_t{1} << q) - 1;
             for (size_t z = 0; z <= full; ++z) {  // a_{~z} == a_z (complement symmetry)
@@ -744,14 +800,15 @@ int qc_top_candidates(qc_engine* e, int q, const double* amps, int top_k, int fo
         auto* st = static_cast<double2*>(e->states.get(N * 16));
         auto* h = static_cast<double*>(e->hstage.get(N * 16));
         std::memcpy(h, amps, N * 16);
-        QC_CUDA(cudaMemcpyAsync(st, h, N * 16, cudaMemcpyHostToDevice, e->stream));
+        e->h2d_copy(st, h, N * 16);
         void* scratch = e->topk_scratch.get(topk_scratch_bytes(q, fold != 0, top_k));
         char* ob = static_cast<char*>(e->topk_out.get(static_cast<size_t>(top_k) * 12 + 64));
         auto* d_bits = reinterpret_cast<uint32_t*>(ob);
         auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(top_k) * 4 + 15) & ~size_t{15}));
-        e->launches += launch_topk(st, q, false, fold != 0, top_k, scratch, d_bits, d_probs, e->stream);
-        QC_CUDA(cudaMemcpyAsync(bits, d_bits, static_cast<size_t>(top_k) * 4, cudaMemcpyDeviceToHost, e->stream));
-        QC_CUDA(cudaMemcpyAsync(probs, d_probs, static_cast<size_t>(top_k) * 8, cudaMemcpyDeviceToHost, e->stream));
+        e->launches += launch_topk(st, q, false, fold != 0, top_k, scratch, d_bits, d_probs, e->stream,
+                                   &e->prof);
+        e->d2h_copy(bits, d_bits, static_cast<size_t>(top_k) * 4);
+        e->d2h_copy(probs, d_probs, static_cast<size_t>(top_k) * 8);
         e->sync();
     });
 }

@@ -62,10 +62,15 @@ struct qc_engine {
     uint64_t mem_budget = 0;
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out;
     qcg::HostBuf hstage, hout;
+    qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
+    uint64_t h2d = 0, d2h = 0;  // bytes copied host<->device by this engine
 
-    // Build the device cut tables of graphs (sym: half state) into `tables`.
+    // Build the device cut tables of graphs (sym: half state) into `target` (default:
+    // the engine's shared `tables` buffer, valid until the next prepare()).
     std::vector<qcg::DevGraph> prepare(const std::vector<qcg::HostGraph>& hg, bool allow_sym,
-                                       bool unit_cost = false);
+                                       bool unit_cost = false, qcg::DevBuf* target = nullptr);
+    void h2d_copy(void* dst, const void* src, size_t bytes);
+    void d2h_copy(void* dst, const void* src, size_t bytes);
     // Evaluate points sharing (q, p) in chunks; out[k] = <C> of point k.
     // flags: qcg::F_* (F_STATE_OUT keeps each chunk's states for `on_chunk`).
     size_t max_slots(int Q, bool onchip) const;
@@ -101,8 +106,13 @@ struct SolveOut {
     double expectation = 0.0;
     int evals = 0;
 };
+void validate_solve(const std::vector<HostGraph>& hg, const std::vector<qc_solve_options>& opts);
 std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
                                   const std::vector<qc_solve_options>& opts);
+// solve on graphs whose device cut tables are already resident (qc_pipeline_*)
+std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>& hg,
+                                     const std::vector<DevGraph>& dg,
+                                     const std::vector<qc_solve_options>& opts);
 
 void set_error(const std::string& msg);
 

@@ -75,18 +75,90 @@ struct ChainPlan {
 };
 ChainPlan plan_chain(int q, bool sym);
 
+// ---------------------------------------------------------------------------
+// Live kernel profiling: CUDA events recorded on the launching stream around each
+// kernel, with the kernel's algorithmic bytes (bench.py roofline).
+// ---------------------------------------------------------------------------
+enum KernelKind : int {
+    K_LEVELS = 0, K_ONCHIP, K_PASS_LOW, K_PASS_HIGH, K_BLOCKSUM, K_FINALSUM, K_TOPK,
+    K_MERGE_TABLES, K_MERGE_SEARCH, K_MERGE_OTHER, K_COUNT
+};
+struct Prof {
+    bool on = false;
+    struct Rec {
+        int kind;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    double ms[K_COUNT] = {};
+    double bytes[K_COUNT] = {};
+    uint64_t count[K_COUNT] = {};
+    cudaEvent_t ev() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void begin(int kind, double b, cudaStream_t s) {
+        if (!on) return;
+        Rec r{kind, ev(), ev(), b};
+        cudaEventRecord(r.a, s);
+        recs.push_back(r);
+    }
+    void end(cudaStream_t s) {
+        if (!on || recs.empty()) return;
+        cudaEventRecord(recs.back().b, s);
+        if (recs.size() >= 4096) resolve();
+    }
+    void resolve() {  // accumulate completed records
+        for (auto& r : recs) {
+            cudaEventSynchronize(r.b);
+            float t = 0.f;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            ms[r.kind] += t;
+            bytes[r.kind] += r.bytes;
+            count[r.kind] += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        recs.clear();
+    }
+    void reset() {
+        resolve();
+        for (int k = 0; k < K_COUNT; ++k) ms[k] = bytes[k] = 0, count[k] = 0;
+    }
+    ~Prof() {
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+};
+
+// Per-layer slot counts of one chain launch (for the algorithmic byte counts).
+struct ChainStats {
+    std::vector<int> phase, mix;  // per layer: slots with the phase / mixer active
+};
+
 // Launchers (qc_kernels.cu). All asynchronous on `stream`; return #kernels launched.
 int launch_levels(const uint32_t* d_eu, const uint32_t* d_ev, const double* d_ew, int m,
                   int Q, bool integral, uint16_t* d_lev, double* d_val, cudaStream_t stream);
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
                  int n_slots, int p, uint32_t flags, double* d_partials, double* d_out,
-                 cudaStream_t stream);
+                 cudaStream_t stream, const ChainStats* stats = nullptr, Prof* prof = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
 
 // Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,
 // ordered by (prob desc, lex asc) (qaoa.hpp:179-182). d_scratch sized by topk_scratch_bytes.
 size_t topk_scratch_bytes(int q, bool fold, int k);
 int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
-                uint32_t* d_bits, double* d_probs, cudaStream_t stream);
+                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof = nullptr);
 
 }  // namespace qcg

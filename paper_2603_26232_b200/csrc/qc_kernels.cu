@@ -24,6 +24,7 @@
 // Q <= 12 (k_onchip): the whole state lives in one CTA's shared memory for all layers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "qc_internal.hpp"
@@ -510,21 +511,28 @@ size_t partials_per_slot(const ChainPlan& plan) {
 
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
                  int n_slots, int p, uint32_t flags, double* d_partials, double* d_out,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, const ChainStats* stats, Prof* prof) {
     if (n_slots <= 0) return 0;
     const int Q = plan.Q;
+    const double N = static_cast<double>(size_t{1} << Q);
     const uint32_t symf = plan.sym ? F_SYM : 0u;
+    auto cnt = [&](const std::vector<int>* v, int l) {
+        return (stats && v && l < static_cast<int>(v->size())) ? (*v)[static_cast<size_t>(l)] : n_slots;
+    };
     if (plan.onchip) {
-        const size_t N = size_t{1} << Q;
-        const size_t smem = N * sizeof(double2) + ((flags & F_EXPECT) ? N * sizeof(double) : 0);
+        const size_t Ns = size_t{1} << Q;
+        const size_t smem = Ns * sizeof(double2) + ((flags & F_EXPECT) ? Ns * sizeof(double) : 0);
         static bool attr_done = false;
         if (!attr_done) {
             QC_CUDA(cudaFuncSetAttribute(k_onchip, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (1 << 12) * 24));
             attr_done = true;
         }
+        const double b = n_slots * N * (((flags & F_INIT) ? 0.0 : 16.0) + ((flags & F_STATE_OUT) ? 16.0 : 0.0));
+        if (prof) prof->begin(K_ONCHIP, b, stream);
         k_onchip<<<n_slots, kOnchipThreads, smem, stream>>>(d_slots, d_lp, p, Q, flags | symf,
                                                             d_out);
+        if (prof) prof->end(stream);
         QC_CUDA(cudaGetLastError());
         return 1;
     }
@@ -539,15 +547,29 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     const unsigned high_grid = static_cast<unsigned>(n_slots) << (Q - 11);
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
+        const int nph = cnt(stats ? &stats->phase : nullptr, l);
+        const int nmix = cnt(stats ? &stats->mix : nullptr, l);
+        // pass A moves a slot if it initialises, phases or mixes it; levels read when phased
+        const int active = fa ? n_slots : std::max(nph, nmix);
+        const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
+        if (prof) prof->begin(K_PASS_LOW, ba, stream);
         k_pass_low<<<low_grid, kLowThreads, 4096 * 16, stream>>>(d_slots, d_lp, l, Q, fa);
+        if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
             const bool last = (l == p - 1) && (h + 1 == plan.high.size());
             uint32_t fh = 0;
             if (last && (flags & F_EXPECT)) fh |= F_EXPECT;
             if (last && (flags & F_STATE_OUT)) fh |= F_STATE_OUT;
+            double bh;
+            if (fh & F_EXPECT)  // read state, write f (+ state), read levels
+                bh = n_slots * N * (16.0 + 8.0 + 2.0 + ((fh & F_STATE_OUT) ? 16.0 : 0.0));
+            else
+                bh = nmix * 32.0 * N;
+            if (prof) prof->begin(K_PASS_HIGH, bh, stream);
             k_pass_high<<<high_grid, kHighThreads, 0, stream>>>(d_slots, d_lp, l, Q, plan.high[h],
                                                                 fh);
+            if (prof) prof->end(stream);
             ++launches;
         }
     }
@@ -555,9 +577,13 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     if (flags & F_EXPECT) {
         const int chains = static_cast<int>(partials_per_slot(plan));
         const int total = chains * n_slots;
+        if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream);
         k_blocksum<<<(total + kSumThreads - 1) / kSumThreads, kSumThreads, 0, stream>>>(
             d_slots, n_slots, Q, plan.sym ? 1 : 0, d_partials);
+        if (prof) prof->end(stream);
+        if (prof) prof->begin(K_FINALSUM, static_cast<double>(total) * 8.0, stream);
         k_finalsum<<<(n_slots + 63) / 64, 64, 0, stream>>>(d_partials, n_slots, chains, d_out);
+        if (prof) prof->end(stream);
         launches += 2;
         QC_CUDA(cudaGetLastError());
     }

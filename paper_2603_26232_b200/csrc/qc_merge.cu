@@ -414,10 +414,15 @@ T* dalloc(std::vector<void*>& keep, size_t n) {
     return static_cast<T*>(p);
 }
 
+thread_local uint64_t* g_h2d_counter = nullptr;
+
 template <typename T>
 T* dupload(std::vector<void*>& keep, const std::vector<T>& h, cudaStream_t st) {
     T* d = dalloc<T>(keep, h.size());
-    if (!h.empty()) QC_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (!h.empty()) {
+        QC_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+        if (g_h2d_counter) *g_h2d_counter += h.size() * sizeof(T);
+    }
     return d;
 }
 
@@ -458,7 +463,12 @@ double estimate_paths(const int32_t* counts, int M, bool halve) {
 }
 
 MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
-                      cudaStream_t st, uint64_t* launches) {
+                      cudaStream_t st, uint64_t* launches, Prof* prof, uint64_t* h2d, uint64_t* d2h) {
+    Prof dummy;
+    if (!prof) prof = &dummy;
+    uint64_t h2d_local = 0, d2h_local = 0;
+    if (!h2d) h2d = &h2d_local;
+    if (!d2h) d2h = &d2h_local;
     const int M = in.levels;
     const int n = in.n;
     std::vector<void*> keep;
@@ -466,8 +476,10 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         std::vector<void*>* k;
         ~Freer() {
             for (void* p : *k) cudaFree(p);
+            g_h2d_counter = nullptr;
         }
     } freer{&keep};
+    g_h2d_counter = h2d;
     auto S = [](int i) { return static_cast<size_t>(i); };
 
     // ---- first level of every vertex (merge.hpp:106-108), integrality
@@ -627,14 +639,18 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         d_ptab = dalloc<int64_t>(keep, static_cast<size_t>(ptab_size));
         if (!gi.empty()) {
             auto* d_gi = dupload(keep, gi, st);
+            prof->begin(K_MERGE_TABLES, static_cast<double>(flat.size()) * 16.0, st);
             k_pair_tables<<<static_cast<unsigned>(gi.size()), 128, 0, st>>>(d_gi, d_pe, d_bits0, d_boff,
                                                                            d_counts, d_intra);
+            prof->end(st);
             ++*launches;
         }
         if (!gp.empty()) {
             auto* d_gp = dupload(keep, gp, st);
+            prof->begin(K_MERGE_TABLES, static_cast<double>(ptab_size) * 8.0, st);
             k_pair_tables<<<static_cast<unsigned>(gp.size()), 128, 0, st>>>(d_gp, d_pe, d_bits0, d_boff,
                                                                            d_counts, d_ptab);
+            prof->end(st);
             ++*launches;
         }
         QC_CUDA(cudaGetLastError());
@@ -740,12 +756,20 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         A.blk_val = d_bval;
         A.blk_ival = d_bival;
         if (integral) {
+            prof->begin(K_MERGE_OTHER, 0.0, st);
             k_unary<<<static_cast<unsigned>(A.L), 128, 0, st>>>(A, d_intra, d_fixed_edges, d_utab);
+            prof->end(st);
+            prof->begin(K_MERGE_SEARCH, static_cast<double>(geo[w].bound) * 8.0, st);
             k_search<true><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
+            prof->end(st);
         } else {
+            prof->begin(K_MERGE_SEARCH, static_cast<double>(geo[w].bound) * 8.0, st);
             k_search<false><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
+            prof->end(st);
         }
+        prof->begin(K_MERGE_OTHER, 0.0, st);
         k_commit<<<1, 1, 0, st>>>(A, static_cast<int>(geo[w].blocks), d_leaves, d_dead, d_acc, d_iacc);
+        prof->end(st);
         *launches += integral ? 3 : 2;
         QC_CUDA(cudaGetLastError());
     }
@@ -756,6 +780,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     QC_CUDA(cudaMemcpyAsync(out.assignment.data(), d_asg, S(n), cudaMemcpyDeviceToHost, st));
     QC_CUDA(cudaMemcpyAsync(&out.leaves, d_leaves, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
     QC_CUDA(cudaMemcpyAsync(&dead, d_dead, sizeof(int), cudaMemcpyDeviceToHost, st));
+    *d2h += S(n) + sizeof(uint64_t) + sizeof(int);
     if (integral && in.m > 0) {
         // cut_value re-score on the device (exact for integral weights)
         std::vector<uint32_t> eu(S(static_cast<int>(in.m))), ev(eu.size());
@@ -771,10 +796,13 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         auto* d_cut = dalloc<unsigned long long>(keep, 1);
         QC_CUDA(cudaMemsetAsync(d_cut, 0, sizeof(unsigned long long), st));
         const long long blocks = std::min<long long>((in.m + 255) / 256, 148 * 8);
+        prof->begin(K_MERGE_OTHER, static_cast<double>(in.m) * 16.0, st);
         k_cut_int<<<static_cast<unsigned>(blocks), 256, 0, st>>>(d_eu, d_ev, d_ew, in.m, d_asg, d_cut);
+        prof->end(st);
         ++*launches;
         unsigned long long cut = 0;
         QC_CUDA(cudaMemcpyAsync(&cut, d_cut, sizeof cut, cudaMemcpyDeviceToHost, st));
+        *d2h += sizeof cut;
         QC_CUDA(cudaStreamSynchronize(st));
         out.value = static_cast<double>(cut);
     } else {

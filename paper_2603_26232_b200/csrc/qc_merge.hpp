@@ -42,7 +42,9 @@ void check_pool(const MergeInput& in);
 double estimate_paths(const int32_t* counts, int M, bool halve);
 // Runs the windows back to back on `st` and returns the re-scored result.
 // full_graph selects MergeEval::kFullGraph scoring (merge.hpp:164) on the exact path.
+struct Prof;
 MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
-                      cudaStream_t st, uint64_t* launches);
+                      cudaStream_t st, uint64_t* launches, Prof* prof = nullptr,
+                      uint64_t* h2d = nullptr, uint64_t* d2h = nullptr);
 
 }  // namespace qcg

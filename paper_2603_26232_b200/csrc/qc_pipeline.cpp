@@ -4,6 +4,7 @@
 // points and the fixed-size solve records used by the multi-GPU gather.
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -193,7 +194,8 @@ MergeOutput level_merge(qc_engine* e, const MergeInput& in, int start_level, int
     if (prefix_est > static_cast<double>(size_t{1} << 22))
         resource_error("start level " + std::to_string(start_level) + " expands to about " +
                        std::to_string(prefix_est) + " prefixes; lower it");
-    return run_merge(in, {Window{0, M, halve ? 3 : 2}}, !incremental, e->stream, &e->launches);
+    return run_merge(in, {Window{0, M, halve ? 3 : 2}}, !incremental, e->stream, &e->launches,
+                     &e->prof, &e->h2d, &e->d2h);
 }
 
 // merge.hpp:345-412 chained_merge
@@ -227,7 +229,7 @@ MergeOutput chained_merge(qc_engine* e, const MergeInput& in, long long window,
         wins.push_back({s, e_, s == 0 ? (halve ? 3 : 2) : -1});
         s = e_;
     }
-    return run_merge(in, wins, false, e->stream, &e->launches);
+    return run_merge(in, wins, false, e->stream, &e->launches, &e->prof, &e->h2d, &e->d2h);
 }
 
 Pool pool_from_c(const qc_pool* p) {
@@ -433,6 +435,88 @@ int qc_run_pipeline(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
         if (report) *report = r;
         write_assignment(out.assignment, assignment);
     });
+}
+
+}  // extern "C"
+
+struct qc_pipeline {
+    qc_engine* e = nullptr;
+    qc_run_config cfg{};
+    HostGraph g;
+    Partition P;
+    std::vector<qc_solve_options> opts;
+    qcg::DevBuf tables;  // resident device cut tables of every subgraph
+    std::vector<DevGraph> dg;
+    double partition_s = 0.0;
+};
+
+extern "C" {
+
+int qc_pipeline_prepare(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
+                        qc_pipeline** out) {
+    return guarded([&] {
+        if (!e || !out) config_error("null argument");
+        QC_CUDA(cudaSetDevice(e->device));
+        check_config(cfg);
+        if (cfg->shard_count != 1) config_error("qc_pipeline_* is single-shard");
+        auto pl = std::make_unique<qc_pipeline>();
+        pl->e = e;
+        pl->cfg = *cfg;
+        pl->g = load_graph(g);
+        auto t0 = std::chrono::steady_clock::now();
+        const int M = cfg->subgraphs != 0 ? cfg->subgraphs : derive_subgraph_count(pl->g.n, cfg->qubit_cap);
+        pl->P = partition(pl->g, M, cfg->partition_mode, cfg->qubit_cap);
+        pl->partition_s = seconds_since(t0);
+        for (int idx = 0; idx < M; ++idx) {
+            const HostGraph& L = pl->P.local[static_cast<size_t>(idx)];
+            const uint64_t classes = cfg->fold ? (uint64_t{1} << (L.n - 1)) : (uint64_t{1} << L.n);
+            qc_solve_options so{};
+            so.top_k = cfg->top_k == 0 ? static_cast<int>(classes)
+                                       : static_cast<int>(std::min<uint64_t>(classes, static_cast<uint64_t>(cfg->top_k)));
+            so.layers = cfg->layers;
+            so.budget = cfg->budget;
+            so.seed = cfg->seed + static_cast<uint64_t>(idx);
+            so.fold = cfg->fold;
+            so.qubit_cap = static_cast<uint64_t>(cfg->qubit_cap);
+            so.tolerance = cfg->nm_tolerance;
+            pl->opts.push_back(so);
+        }
+        validate_solve(pl->P.local, pl->opts);
+        pl->dg = e->prepare(pl->P.local, true, false, &pl->tables);
+        *out = pl.release();
+    });
+}
+
+int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment) {
+    return guarded([&] {
+        if (!pl) config_error("null pipeline");
+        qc_engine* e = pl->e;
+        QC_CUDA(cudaSetDevice(e->device));
+        qc_run_report r{};
+        r.partition_s = pl->partition_s;
+        r.subgraphs = static_cast<int32_t>(pl->P.first.size());
+        auto t0 = std::chrono::steady_clock::now();
+        const auto solves = solve_prepared(e, pl->P.local, pl->dg, pl->opts);
+        r.qaoa_s = seconds_since(t0);
+        for (const auto& s : solves) r.evals += static_cast<uint64_t>(s.evals);
+        t0 = std::chrono::steady_clock::now();
+        bool windowed = false;
+        const MergeOutput out = merge_stage(e, pl->g, pl->P, solves, &pl->cfg, &windowed);
+        r.merge_s = seconds_since(t0);
+        r.total_s = r.partition_s + r.qaoa_s + r.merge_s;
+        r.cut = out.value;
+        r.candidates_evaluated = out.leaves;
+        r.windowed = windowed ? 1 : 0;
+        if (report) *report = r;
+        write_assignment(out.assignment, assignment);
+    });
+}
+
+void qc_pipeline_destroy(qc_pipeline* pl) {
+    if (!pl) return;
+    cudaSetDevice(pl->e->device);
+    cudaStreamSynchronize(pl->e->stream);
+    delete pl;
 }
 
 int64_t qc_record_bytes(int top_k_cap, int layers) { return record_bytes(top_k_cap, layers); }

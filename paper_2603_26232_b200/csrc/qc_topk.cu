@@ -188,8 +188,17 @@ size_t topk_scratch_bytes(int q, bool fold, int k) {
 }
 
 int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
-                uint32_t* d_bits, double* d_probs, cudaStream_t stream) {
+                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof) {
     const uint64_t classes = class_count(q, fold);
+    const double sbytes = static_cast<double>(sym ? (uint64_t{1} << (q - 1)) : (uint64_t{1} << q)) * 16.0;
+    if (prof) prof->begin(K_TOPK, sbytes, stream);
+    struct End {
+        Prof* p;
+        cudaStream_t s;
+        ~End() {
+            if (p) p->end(s);
+        }
+    } end_guard{prof, stream};
     Key* keys = static_cast<Key*>(d_scratch);
     int launches = 0;
     if (k > kChunk / 2) {
