@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numbers>
@@ -187,19 +188,48 @@ double2* qc_engine::slot_state(int q, bool sym, int k) {
 
 void qc_engine::sync() { QC_CUDA(cudaStreamSynchronize(stream)); }
 
-void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
-                           uint32_t flags, double* out) {
+size_t qc_engine::chunk_slots(int Q, bool onchip, size_t n) const {
+    if (const char* env = std::getenv("QCG_CHUNK_SLOTS")) {
+        const long v = std::strtol(env, nullptr, 10);
+        if (v > 0) return std::min<size_t>(n, static_cast<size_t>(v));
+    }
+    if (onchip) return std::max<size_t>(1, (n + 1) / 2);  // two chunks: host/device overlap
+    const size_t per = (size_t{1} << Q) * 26;              // state 16 + f 8 + levels 2 B/amp
+    const size_t l2_target = size_t{96} << 20;              // of the 126 MB L2
+    size_t g = std::max<size_t>(1, l2_target / per);
+    const size_t chunks = (n + g - 1) / g;
+    return (n + chunks - 1) / chunks;                        // balance the chunks
+}
+
+void qc_engine::reserve(int Q, bool need_fbuf, size_t slots) {
+    const size_t N = size_t{1} << Q;
+    states.get(slots * N * 16);
+    if (need_fbuf) fbuf.get(slots * N * 8);
+    const size_t pps = Q > 12 ? (size_t{2} << (Q - 12)) : 0;
+    partials.get(slots * pps * 8 + 8);
+    outd.get(slots * 8);
+    if (tickets.cap < slots * 4) {  // zeroed once; kernels leave them zeroed
+        tickets.get(slots * 4);
+        QC_CUDA(cudaMemsetAsync(tickets.p, 0, tickets.cap, stream));
+    }
+}
+
+void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
+                              uint32_t flags, size_t slot0, ChunkCtx& ctx) {
+    ctx.n = n;
+    ctx.flags = flags;
     if (n <= 0) return;
     const DevGraph& g0 = dg[static_cast<size_t>(pts[0].g)];
     const ChainPlan plan = plan_chain(g0.q, g0.sym);
     const size_t N = size_t{1} << plan.Q;
-    auto* st = static_cast<double2*>(states.get(static_cast<size_t>(n) * N * 16));
+    auto* st = static_cast<double2*>(states.p) + slot0 * N;
     double* fb = nullptr;
-    if (!plan.onchip && (flags & F_EXPECT))
-        fb = static_cast<double*>(fbuf.get(static_cast<size_t>(n) * N * 8));
+    if (!plan.onchip && (flags & F_EXPECT)) fb = static_cast<double*>(fbuf.p) + slot0 * N;
     const size_t pps = partials_per_slot(plan);
-    auto* part = static_cast<double*>(partials.get(static_cast<size_t>(n) * pps * 8 + 8));
-    auto* od = static_cast<double*>(outd.get(static_cast<size_t>(n) * 8));
+    auto* part = static_cast<double*>(partials.p) + slot0 * pps;
+    auto* tick = static_cast<unsigned*>(tickets.p) + slot0;
+    auto* od = static_cast<double*>(outd.p) + slot0;
+    ctx.d_out = od;
 
     // staging: [SlotDesc n][LayerParam n*p][LUT entries]
     size_t lut_total = 0;
@@ -214,8 +244,8 @@ void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts
         (o_lp + static_cast<size_t>(n) * static_cast<size_t>(std::max(p, 1)) * sizeof(LayerParam) + 255) &
         ~size_t{255};
     const size_t bytes = o_lut + lut_total * 16;
-    char* h = static_cast<char*>(hstage.get(bytes));
-    char* d = static_cast<char*>(stage.get(bytes));
+    char* h = static_cast<char*>(ctx.hstage.get(bytes));
+    char* d = static_cast<char*>(ctx.dstage.get(bytes));
     auto* hs = reinterpret_cast<SlotDesc*>(h);
     auto* hl = reinterpret_cast<LayerParam*>(h + o_lp);
     auto* hlut = reinterpret_cast<double*>(h + o_lut);
@@ -262,16 +292,30 @@ void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts
     }
     h2d_copy(d, h, bytes);
     launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
-                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, part, od,
-                             stream, &stats, &prof);
+                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, part,
+                             tick, od, stream, &stats, &prof);
     if (flags & F_EXPECT) {
-        auto* ho = static_cast<double*>(hout.get(static_cast<size_t>(n) * 8));
+        auto* ho = static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8));
         d2h_copy(ho, od, static_cast<size_t>(n) * 8);
-        QC_CUDA(cudaStreamSynchronize(stream));
-        std::memcpy(out, ho, static_cast<size_t>(n) * 8);
-    } else {
-        QC_CUDA(cudaStreamSynchronize(stream));
     }
+    if (!ctx.done) QC_CUDA(cudaEventCreateWithFlags(&ctx.done, cudaEventDisableTiming));
+    QC_CUDA(cudaEventRecord(ctx.done, stream));
+}
+
+void qc_engine::wait_chunk(ChunkCtx& ctx, double* out) {
+    if (ctx.n <= 0) return;
+    QC_CUDA(cudaEventSynchronize(ctx.done));
+    if ((ctx.flags & F_EXPECT) && out) std::memcpy(out, ctx.hout.p, static_cast<size_t>(ctx.n) * 8);
+}
+
+void qc_engine::eval_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
+                           uint32_t flags, double* out) {
+    if (n <= 0) return;
+    const DevGraph& g0 = dg[static_cast<size_t>(pts[0].g)];
+    const ChainPlan plan = plan_chain(g0.q, g0.sym);
+    reserve(plan.Q, !plan.onchip && (flags & F_EXPECT), static_cast<size_t>(n));
+    enqueue_chunk(dg, pts, n, p, flags, 0, sync_ctx);
+    wait_chunk(sync_ctx, out);
 }
 
 void qc_engine::eval(const std::vector<DevGraph>& dg, const std::vector<EvalPoint>& pts, int p,
@@ -313,30 +357,63 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
         if (layers[i] < 1) config_error("layer count must be positive");      // qaoa.hpp:28
         opt[i].start(layers[i], budget[i], seeds[i], tol[i]);
     }
-    // one lockstep step: every live optimiser asks one point; points grouped by p
-    std::vector<EvalPoint> pts;
-    std::vector<int> who;
-    std::vector<double> vals;
-    std::map<int, std::vector<size_t>> by_p;
-    for (;;) {
-        by_p.clear();
-        for (size_t i = 0; i < n; ++i)
-            if (!opt[i].done()) by_p[layers[i]].push_back(i);
-        if (by_p.empty()) break;
-        for (auto& [p, ids] : by_p) {
-            pts.clear();
-            for (size_t i : ids) pts.push_back({static_cast<int>(i), opt[i].point().data()});
-            vals.assign(pts.size(), 0.0);
-            e->eval(dg, pts, p, vals.data());
-            for (size_t k = 0; k < ids.size(); ++k) {
-                const size_t i = ids[k];
-                const double f = -vals[k];  // qaoa.hpp:90
-                if (trace_x) {
-                    const auto& x = opt[i].point();
-                    (*trace_x)[i].insert((*trace_x)[i].end(), x.begin(), x.end());
-                    (*trace_f)[i].push_back(f);
+    // Tasks sharing (q, p) run as one lockstep group. The group is cut into chunks whose
+    // working set fits L2; chunk c's next step is prepared on the host while the device
+    // runs the chunks queued behind it (results are placement independent: every
+    // evaluation restarts from |+>).
+    std::map<std::pair<int, int>, std::vector<size_t>> groups;
+    for (size_t i = 0; i < n; ++i) groups[{dg[i].q, layers[i]}].push_back(i);
+    for (auto& [key, tasks] : groups) {
+        const int p = key.second;
+        const ChainPlan plan = plan_chain(dg[tasks[0]].q, dg[tasks[0]].sym);
+        const size_t cap = e->max_slots(plan.Q, plan.onchip);
+        for (size_t sb = 0; sb < tasks.size(); sb += cap) {
+            const size_t se = std::min(tasks.size(), sb + cap);
+            const size_t ns = se - sb;
+            const size_t per = e->chunk_slots(plan.Q, plan.onchip, ns);
+            const size_t nchunks = (ns + per - 1) / per;
+            e->reserve(plan.Q, !plan.onchip, ns);
+            std::vector<ChunkCtx> ctx(nchunks);
+            std::vector<std::vector<EvalPoint>> pts(nchunks);
+            std::vector<std::vector<size_t>> who(nchunks);
+            std::vector<char> inflight(nchunks, 0);
+            std::vector<double> vals;
+            auto launch = [&](size_t c) {
+                pts[c].clear();
+                who[c].clear();
+                const size_t b = sb + c * per, end = std::min(se, b + per);
+                for (size_t k = b; k < end; ++k) {
+                    const size_t i = tasks[k];
+                    if (opt[i].done()) continue;
+                    pts[c].push_back({static_cast<int>(i), opt[i].point().data()});
+                    who[c].push_back(i);
                 }
-                opt[i].tell(f);
+                inflight[c] = !pts[c].empty();
+                if (inflight[c])
+                    e->enqueue_chunk(dg, pts[c].data(), static_cast<int>(pts[c].size()), p,
+                                     F_INIT | F_EXPECT, c * per, ctx[c]);
+            };
+            for (size_t c = 0; c < nchunks; ++c) launch(c);
+            bool any = true;
+            while (any) {
+                any = false;
+                for (size_t c = 0; c < nchunks; ++c) {
+                    if (!inflight[c]) continue;
+                    vals.assign(pts[c].size(), 0.0);
+                    e->wait_chunk(ctx[c], vals.data());
+                    for (size_t k = 0; k < who[c].size(); ++k) {
+                        const size_t i = who[c][k];
+                        const double f = -vals[k];  // qaoa.hpp:90
+                        if (trace_x) {
+                            const auto& x = opt[i].point();
+                            (*trace_x)[i].insert((*trace_x)[i].end(), x.begin(), x.end());
+                            (*trace_f)[i].push_back(f);
+                        }
+                        opt[i].tell(f);
+                    }
+                    launch(c);
+                    any = any || inflight[c];
+                }
             }
         }
     }

@@ -53,6 +53,22 @@ struct EvalPoint {
     const double* x;  // packed [gammas..., betas...]
 };
 
+// Staging + completion event of one in-flight launch chain ("chunk" of slots).
+struct ChunkCtx {
+    DevBuf dstage;
+    HostBuf hstage, hout;
+    cudaEvent_t done = nullptr;
+    int n = 0;
+    uint32_t flags = 0;
+    double* d_out = nullptr;
+    ChunkCtx() = default;
+    ChunkCtx(const ChunkCtx&) = delete;
+    ChunkCtx& operator=(const ChunkCtx&) = delete;
+    ~ChunkCtx() {
+        if (done) cudaEventDestroy(done);
+    }
+};
+
 }  // namespace qcg
 
 struct qc_engine {
@@ -60,7 +76,7 @@ struct qc_engine {
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
     uint64_t mem_budget = 0;
-    qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out;
+    qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
     qcg::HostBuf hstage, hout;
     qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
     uint64_t h2d = 0, d2h = 0;  // bytes copied host<->device by this engine
@@ -74,8 +90,17 @@ struct qc_engine {
     // Evaluate points sharing (q, p) in chunks; out[k] = <C> of point k.
     // flags: qcg::F_* (F_STATE_OUT keeps each chunk's states for `on_chunk`).
     size_t max_slots(int Q, bool onchip) const;
+    // Slots per pipelined chunk: sized so a chunk's working set stays L2-resident.
+    size_t chunk_slots(int Q, bool onchip, size_t n) const;
+    // Grow the shared slot buffers to `slots` slots of 2^Q (no work may be in flight).
+    void reserve(int Q, bool need_fbuf, size_t slots);
+    // Asynchronous chain on slots [slot0, slot0+n); wait_chunk collects <C> (F_EXPECT).
+    void enqueue_chunk(const std::vector<qcg::DevGraph>& dg, const qcg::EvalPoint* pts, int n,
+                       int p, uint32_t flags, size_t slot0, qcg::ChunkCtx& c);
+    void wait_chunk(qcg::ChunkCtx& c, double* out);
     void eval_chunk(const std::vector<qcg::DevGraph>& dg, const qcg::EvalPoint* pts, int n, int p,
                     uint32_t flags, double* out);
+    qcg::ChunkCtx sync_ctx;
     void eval(const std::vector<qcg::DevGraph>& dg, const std::vector<qcg::EvalPoint>& pts, int p,
               double* out);
     double2* slot_state(int q, bool sym, int k);

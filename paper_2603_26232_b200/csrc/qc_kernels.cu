@@ -20,7 +20,7 @@
 //   pass A  (k_pass_low):  2^12 contiguous amps per CTA, [init |+>] + phase + RX 0..11
 //   pass Bk (k_pass_high): 8 gather bits x 8-amp columns per CTA, RX on bits >= 12,
 //                          mirror op last; the final one emits f(z)=|a|^2 C(z)
-//   k_blocksum / k_finalsum: the blocked sequential expectation over f.
+//   k_blocksum: the blocked sequential expectation over f (+ the in-order block sum).
 // Q <= 12 (k_onchip): the whole state lives in one CTA's shared memory for all layers.
 #include <cuda_runtime.h>
 
@@ -221,11 +221,28 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const SlotDesc* __res
 }
 
 // ---------------------------------------------------------------------------
-// k_pass_low: pass A, 4096 contiguous stored amplitudes, targets 0..11.
-// 256 threads x 16 amplitudes; three register rounds of 4 targets, exchanged
-// through an XOR-swizzled shared tile (conflict-free 16-byte accesses).
+// cp.async (LDGSTS) helpers: 16-byte global->shared copies that bypass registers, so a
+// persistent CTA streams its next tile in while it computes the current one.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void bar_named(int id, int n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// k_pass_low: pass A, 4096 contiguous stored amplitudes per tile, targets 0..11.
+// Persistent: one 256-thread CTA per SM walks tiles blockIdx.x, +gridDim.x, ...;
+// tile k+1 (amplitudes + cut levels) is prefetched with cp.async into the other
+// stage while tile k runs three register rounds of 4 targets (16 amps/thread)
+// exchanged through an XOR-swizzled stage (conflict-free 16-byte accesses).
 // ---------------------------------------------------------------------------
 constexpr int kLowThreads = 256;
+constexpr size_t kLowSmem = 2 * 4096 * sizeof(double2) + 2 * 4096 * sizeof(uint16_t);
 
 __device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 7u); }
 
@@ -239,72 +256,105 @@ __device__ __forceinline__ void rx_local4(double2 (&a)[16], double c, double s) 
     }
 }
 
-__global__ void __launch_bounds__(kLowThreads, 2) k_pass_low(const SlotDesc* __restrict__ slots,
+__global__ void __launch_bounds__(kLowThreads, 1) k_pass_low(const SlotDesc* __restrict__ slots,
                                                            const LayerParam* __restrict__ lp,
-                                                           int layer, int Q, uint32_t flags) {
-    extern __shared__ double2 sm[];
+                                                           int layer, int Q, uint32_t flags,
+                                                           uint32_t total_tiles) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    double2* buf = reinterpret_cast<double2*>(smraw);                       // [2][4096]
+    uint16_t* levs = reinterpret_cast<uint16_t*>(smraw + 2 * 4096 * sizeof(double2));  // [2][4096]
     const int tshift = Q - 12;
-    const int slot = blockIdx.x >> tshift;
-    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
-    const SlotDesc S = slots[slot];
-    const LayerParam L = lp[S.layer_base + layer];
+    const uint32_t tmask = (1u << tshift) - 1u;
     const bool init = flags & F_INIT;
-    if (!init && !L.phase && !L.mix) return;  // identity layer: memory already holds it
-    const uint32_t base = tile << 12;
-    double2* __restrict__ st = S.state + base;
     const uint32_t tid = threadIdx.x;
-    double2 a[16];
 
-    if (init) {
+    auto issue = [&](uint32_t t, int stage) {
+        if (t < total_tiles) {
+            const SlotDesc& S = slots[t >> tshift];
+            const LayerParam& L = lp[S.layer_base + layer];
+            if (init || L.phase || L.mix) {
+                const uint32_t base = (t & tmask) << 12;
+                if (!init) {
+                    const double2* src = S.state + base;
+                    double2* dst = buf + stage * 4096;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t e = tid * 16u + j;
-            double2 v = make_double2(S.amp0, 0.0);
-            if (L.phase) v = phase_rn(v, S, L, base + e);
-            a[j] = v;
+                    for (int k = 0; k < 16; ++k)
+                        cp_async16(dst + swz(k * kLowThreads + tid), src + k * kLowThreads + tid);
+                }
+                if (L.phase && S.lev) {
+                    const uint16_t* src = S.lev + base;
+                    uint16_t* dst = levs + stage * 4096;
+                    cp_async16(dst + tid * 8, src + tid * 8);
+                    cp_async16(dst + (tid + 256) * 8, src + (tid + 256) * 8);
+                }
+            }
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) a[k] = st[k * kLowThreads + tid];
-        if (L.phase) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) a[k] = phase_rn(a[k], S, L, base + k * kLowThreads + tid);
-        }
-#pragma unroll
-        for (int k = 0; k < 16; ++k) sm[swz(k * kLowThreads + tid)] = a[k];
+        cp_commit();
+    };
+
+    uint32_t t = blockIdx.x;
+    issue(t, 0);
+    for (int k = 0; t < total_tiles; ++k, t += gridDim.x) {
+        const int stage = k & 1;
+        issue(t + gridDim.x, stage ^ 1);
+        cp_wait1();
         __syncthreads();
+        const SlotDesc S = slots[t >> tshift];
+        const LayerParam L = lp[S.layer_base + layer];
+        if (init || L.phase || L.mix) {  // else: identity layer, memory already holds it
+            const uint32_t base = (t & tmask) << 12;
+            double2* sm = buf + stage * 4096;
+            const uint16_t* lv = levs + stage * 4096;
+            double2 a[16];
+            // round 0: bits 0..3 thread-local (e = tid*16 + j), phase first
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = sm[swz(tid * 16u + j)];
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t e = tid * 16u + j;
+                double2 v = init ? make_double2(S.amp0, 0.0) : sm[swz(e)];
+                if (L.phase) {
+                    if (S.lev)
+                        v = cmul_rn(v, L.lut[lv[e]]);
+                    else
+                        v = phase_rn(v, S, L, base + e);
+                }
+                a[j] = v;
+            }
+            if (L.mix) rx_local4(a, L.c, L.s);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sm[swz(tid * 16u + j)] = a[j];
+            __syncthreads();
+            // round 1: bits 4..7 (e = (tid>>4)<<8 | j<<4 | tid&15)
+            const uint32_t r1 = ((tid >> 4) << 8) | (tid & 15u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = sm[swz(r1 | (j << 4))];
+            if (L.mix) rx_local4(a, L.c, L.s);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sm[swz(r1 | (j << 4))] = a[j];
+            __syncthreads();
+            // round 2: bits 8..11 (e = j<<8 | tid), stored straight back (coalesced)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = sm[swz((j << 8) | tid)];
+            if (L.mix) rx_local4(a, L.c, L.s);
+            double2* st = S.state + base;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[(j << 8) | tid] = a[j];
+        }
+        __syncthreads();  // this stage is refilled by the next iteration's prefetch
     }
-    // round 0: bits 0..3 thread-local (e = tid*16 + j)
-    if (L.mix) rx_local4(a, L.c, L.s);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) sm[swz(tid * 16u + j)] = a[j];
-    __syncthreads();
-    // round 1: bits 4..7 (e = (tid>>4)<<8 | j<<4 | tid&15)
-    const uint32_t r1 = ((tid >> 4) << 8) | (tid & 15u);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = sm[swz(r1 | (j << 4))];
-    if (L.mix) rx_local4(a, L.c, L.s);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) sm[swz(r1 | (j << 4))] = a[j];
-    __syncthreads();
-    // round 2: bits 8..11 (e = j<<8 | tid), stored straight back (coalesced)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = sm[swz((j << 8) | tid)];
-    if (L.mix) rx_local4(a, L.c, L.s);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) st[(j << 8) | tid] = a[j];
 }
 
 // ---------------------------------------------------------------------------
-// k_pass_high: 3 column bits (8 contiguous amps) x 8 tile bits per CTA.
+// k_pass_high: 3 column bits (8 contiguous amps) x 8 tile bits per tile.
 // Tile bit kinds: 1 RX target (mask = one stored bit), 2 mirror (mask = all Q bits,
 // RX on qubit q-1), 0 batch (no op). Targets precede the mirror in tile-bit order.
 // In the mirror half of a tile (mirror bit set) every stored bit is complemented, so
 // the RX roles (a0 = bit clear) of target pairs swap.
+// Persistent: each 256-thread CTA runs two independent 128-thread tile streams
+// (named barriers), each double-buffering its next tile's 128-byte column segments
+// with cp.async.
 // ---------------------------------------------------------------------------
-constexpr int kHighThreads = 128;
+constexpr int kHighThreads = 256;
+constexpr size_t kHighSmem = 2 * 2 * 2048 * sizeof(double2);
 
 template <int OFF>
 __device__ __forceinline__ void high_round(double2 (&a)[16], const HighPass& hp, int mir_local,
@@ -329,129 +379,175 @@ __device__ __forceinline__ void high_round(double2 (&a)[16], const HighPass& hp,
     }
 }
 
-__global__ void __launch_bounds__(kHighThreads, 4) k_pass_high(const SlotDesc* __restrict__ slots,
+__global__ void __launch_bounds__(kHighThreads, 1) k_pass_high(const SlotDesc* __restrict__ slots,
                                                              const LayerParam* __restrict__ lp,
                                                              int layer, int Q, HighPass hp,
-                                                             uint32_t flags) {
-    __shared__ double2 sm[2048];
+                                                             uint32_t flags, uint32_t total_tiles) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int half = threadIdx.x >> 7;
+    double2* hbuf = reinterpret_cast<double2*>(smraw) + half * 2 * 2048;  // [2][2048]
     const int tshift = Q - 11;
-    const int slot = blockIdx.x >> tshift;
-    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
-    const SlotDesc S = slots[slot];
-    const LayerParam L = lp[S.layer_base + layer];
+    const uint32_t tmask = (1u << tshift) - 1u;
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
-    if (!L.mix && !fout) return;
-    const bool mix = L.mix;
-    const uint32_t x = deposit(tile, hp.freemask);
-    const uint32_t tid = threadIdx.x;
-    const uint32_t w = tid & 7u;
-
-    int mpos = -1;  // tile-bit index of the mirror pseudo-bit
+    const uint32_t ht = threadIdx.x & 127u;
+    const uint32_t w = ht & 7u;
+    const uint32_t hb = ht >> 3;  // round 0: tile bits 4..7; round 1: tile bits 0..3
+    int mpos = -1;                // tile-bit index of the mirror pseudo-bit
 #pragma unroll
     for (int k = 0; k < 8; ++k)
         if (hp.kind[k] == 2) mpos = k;
-
-    double2 a[16];
-    // ---- round 0: tile bits 0..3 local; thread = (w, tile bits 4..7 = hi)
-    {
-        const uint32_t hi = tid >> 3;
-        uint32_t gt = x | w;
+    // XOR of the thread's own tile-bit masks
+    uint32_t thr_hi = 0, thr_lo = 0;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if ((hi >> b) & 1u) gt ^= hp.mask[4 + b];
-        const bool mir_t = mpos >= 4 && ((hi >> (mpos - 4)) & 1u);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            uint32_t g = gt;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((j >> b) & 1) g ^= hp.mask[b];
-            a[j] = S.state[g];
-        }
-        if (mix) high_round<0>(a, hp, mpos < 4 ? mpos : -1, mir_t, L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) sm[w | (j << 3) | (hi << 7)] = a[j];
+    for (int b = 0; b < 4; ++b) {
+        if ((hb >> b) & 1u) thr_hi ^= hp.mask[4 + b];
+        if ((hb >> b) & 1u) thr_lo ^= hp.mask[b];
     }
-    __syncthreads();
-    // ---- round 1: tile bits 4..7 local; thread = (w, tile bits 0..3 = lo)
-    {
-        const uint32_t lo = tid >> 3;
-        uint32_t gt = x | w;
+    const uint32_t streams = 2 * gridDim.x;
+
+    auto issue = [&](uint32_t t, int stage) {
+        if (t < total_tiles) {
+            const SlotDesc& S = slots[t >> tshift];
+            const LayerParam& L = lp[S.layer_base + layer];
+            if (L.mix || fout) {
+                const uint32_t gt = deposit(t & tmask, hp.freemask) | w;
+                double2* dst = hbuf + stage * 2048;
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-            if ((lo >> b) & 1u) gt ^= hp.mask[b];
-        const bool mir_t = mpos >= 0 && mpos < 4 && ((lo >> mpos) & 1u);
+                for (int j = 0; j < 16; ++j) {
+                    uint32_t g = gt ^ thr_hi;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = sm[w | (lo << 3) | (j << 7)];
-        if (mix) high_round<4>(a, hp, mpos >= 4 ? mpos - 4 : -1, mir_t, L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            uint32_t g = gt;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if ((j >> b) & 1) g ^= hp.mask[4 + b];
-            if (sout) S.state[g] = a[j];
-            if (fout) S.fbuf[g] = __dmul_rn(norm_rn(a[j]), cost_of(S, g));
+                    for (int b = 0; b < 4; ++b)
+                        if ((j >> b) & 1) g ^= hp.mask[b];
+                    cp_async16(dst + (w | (j << 3) | (hb << 7)), S.state + g);
+                }
+            }
         }
+        cp_commit();
+    };
+
+    uint32_t t = blockIdx.x * 2 + half;
+    issue(t, 0);
+    for (int k = 0; t < total_tiles; ++k, t += streams) {
+        const int stage = k & 1;
+        issue(t + streams, stage ^ 1);
+        cp_wait1();
+        const SlotDesc S = slots[t >> tshift];
+        const LayerParam L = lp[S.layer_base + layer];
+        if (L.mix || fout) {
+            const bool mix = L.mix;
+            const uint32_t gt = deposit(t & tmask, hp.freemask) | w;
+            double2* sm = hbuf + stage * 2048;
+            double2 a[16];
+            // round 0: tile bits 0..3 local; the thread reads exactly what it copied
+            {
+                const bool mir_t = mpos >= 4 && ((hb >> (mpos - 4)) & 1u);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) a[j] = sm[w | (j << 3) | (hb << 7)];
+                if (mix) high_round<0>(a, hp, mpos < 4 ? mpos : -1, mir_t, L.c, L.s);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sm[w | (j << 3) | (hb << 7)] = a[j];
+            }
+            bar_named(1 + half, 128);
+            // round 1: tile bits 4..7 local; thread = (w, tile bits 0..3 = hb)
+            {
+                const bool mir_t = mpos >= 0 && mpos < 4 && ((hb >> mpos) & 1u);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) a[j] = sm[w | (hb << 3) | (j << 7)];
+                if (mix) high_round<4>(a, hp, mpos >= 4 ? mpos - 4 : -1, mir_t, L.c, L.s);
+                const uint32_t g0 = gt ^ thr_lo;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    uint32_t g = g0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if ((j >> b) & 1) g ^= hp.mask[4 + b];
+                    if (sout) S.state[g] = a[j];
+                    if (fout) S.fbuf[g] = __dmul_rn(norm_rn(a[j]), cost_of(S, g));
+                }
+            }
+        }
+        bar_named(1 + half, 128);  // this stage is refilled by the next prefetch
     }
 }
 
 // ---------------------------------------------------------------------------
-// blocked expectation over f (statevector.hpp:48-65): one thread per 4096-block
-// chain. SYM: chain c < nbl is lower block c ascending; c >= nbl is the mirrored
-// upper block 2nbl-1-c, i.e. stored block (2nbl-1-c) descending. Partials land in
-// full-index block order.
+// blocked expectation over f (statevector.hpp:48-65). One warp per stored 4096-block:
+// the warp streams the block through shared memory (coalesced 16-byte loads, double
+// buffered) while lane 0 runs the ascending chain (the block itself) and, in SYM mode,
+// lane 1 the descending chain (its mirror block in the upper half, 2nbl-1-b). Partials
+// land in full-index block order; the last warp of a slot (atomic ticket) sums them in
+// block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
-constexpr int kSumThreads = 64;
+constexpr int kSumWarps = 4;
+constexpr int kSumChunk = 512;  // doubles per chunk
 
-__global__ void __launch_bounds__(kSumThreads) k_blocksum(const SlotDesc* __restrict__ slots,
-                                                        int n_slots, int Q, int sym,
-                                                        double* __restrict__ partials) {
+__global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __restrict__ slots,
+                                                          int n_slots, int Q, int sym,
+                                                          double* __restrict__ partials,
+                                                          unsigned* __restrict__ tickets,
+                                                          double* __restrict__ out) {
+    extern __shared__ double sbuf[];  // [warp][2 stages][fwd, bwd][kSumChunk]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nbl = 1 << (Q - 12);
     const int chains = sym ? 2 * nbl : nbl;
-    const int gid = blockIdx.x * kSumThreads + threadIdx.x;
-    const int slot = gid / chains;
+    const int gw = blockIdx.x * kSumWarps + warp;
+    const int slot = gw / nbl;
     if (slot >= n_slots) return;
-    const int c = gid - slot * chains;
-    const double2* f2 = reinterpret_cast<const double2*>(slots[slot].fbuf);
+    const int b = gw - slot * nbl;
+    const double2* f2 = reinterpret_cast<const double2*>(slots[slot].fbuf + (size_t)b * kBlock);
+    double* wb = sbuf + (size_t)warp * 2 * 2 * kSumChunk;
+    constexpr int kPer = kSumChunk / 2 / 32;  // double2 per lane per chunk
+    constexpr int kChunks = kBlock / kSumChunk;
+    double2 rf[kPer], rb[kPer];
+    auto load = [&](int c) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) rf[u] = f2[c * (kSumChunk / 2) + u * 32 + lane];
+        if (sym)
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) rb[u] = f2[(kChunks - 1 - c) * (kSumChunk / 2) + u * 32 + lane];
+    };
+    auto stash = [&](int stage) {
+        double2* d = reinterpret_cast<double2*>(wb + stage * 2 * kSumChunk);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) d[u * 32 + lane] = rf[u];
+        if (sym)
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) d[kSumChunk / 2 + u * 32 + lane] = rb[u];
+    };
+    load(0);
+    stash(0);
+    __syncwarp();
     double acc = 0.0;
-    if (c < nbl) {
-        const double2* p = f2 + (size_t)c * (kBlock / 2);
-        for (int k = 0; k < kBlock / 2; k += 8) {
-            double2 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = p[k + u];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                acc = __dadd_rn(acc, v[u].x);
-                acc = __dadd_rn(acc, v[u].y);
-            }
+    for (int c = 0; c < kChunks; ++c) {
+        if (c + 1 < kChunks) load(c + 1);  // in flight while the chains run
+        const double* cur = wb + (c & 1) * 2 * kSumChunk;
+        if (lane == 0) {
+#pragma unroll 16
+            for (int k = 0; k < kSumChunk; ++k) acc = __dadd_rn(acc, cur[k]);
+        } else if (lane == 1 && sym) {
+#pragma unroll 16
+            for (int k = kSumChunk - 1; k >= 0; --k) acc = __dadd_rn(acc, cur[kSumChunk + k]);
         }
-    } else {
-        const double2* p = f2 + (size_t)(2 * nbl - 1 - c) * (kBlock / 2);
-        for (int k = kBlock / 2 - 8; k >= 0; k -= 8) {
-            double2 v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = p[k + u];
-#pragma unroll
-            for (int u = 7; u >= 0; --u) {
-                acc = __dadd_rn(acc, v[u].y);
-                acc = __dadd_rn(acc, v[u].x);
-            }
+        __syncwarp();
+        if (c + 1 < kChunks) stash((c + 1) & 1);
+        __syncwarp();
+    }
+    double* pp = partials + (size_t)slot * chains;
+    if (lane == 0) pp[b] = acc;
+    if (lane == 1 && sym) pp[2 * nbl - 1 - b] = acc;
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        const unsigned ticket = atomicAdd(&tickets[slot], 1u);
+        if (ticket == static_cast<unsigned>(nbl - 1)) {  // last block of this slot
+            __threadfence();
+            double total = 0.0;
+            for (int k = 0; k < chains; ++k) total = __dadd_rn(total, __ldcg(pp + k));
+            out[slot] = total;
+            tickets[slot] = 0u;
         }
     }
-    partials[(size_t)slot * chains + c] = acc;
-}
-
-__global__ void k_finalsum(const double* __restrict__ partials, int n_slots, int chains,
-                           double* __restrict__ out) {
-    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= n_slots) return;
-    const double* p = partials + (size_t)slot * chains;
-    double total = 0.0;
-    for (int c = 0; c < chains; ++c) total = __dadd_rn(total, p[c]);
-    out[slot] = total;
 }
 
 // ---------------------------------------------------------------------------
@@ -510,8 +606,8 @@ size_t partials_per_slot(const ChainPlan& plan) {
 }
 
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
-                 int n_slots, int p, uint32_t flags, double* d_partials, double* d_out,
-                 cudaStream_t stream, const ChainStats* stats, Prof* prof) {
+                 int n_slots, int p, uint32_t flags, double* d_partials, unsigned* d_tickets,
+                 double* d_out, cudaStream_t stream, const ChainStats* stats, Prof* prof) {
     if (n_slots <= 0) return 0;
     const int Q = plan.Q;
     const double N = static_cast<double>(size_t{1} << Q);
@@ -536,15 +632,21 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         QC_CUDA(cudaGetLastError());
         return 1;
     }
-    static bool low_attr = false;
-    if (!low_attr) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QC_CUDA(cudaGetDevice(&dev));
+        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         QC_CUDA(cudaFuncSetAttribute(k_pass_low, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     4096 * 16));
-        low_attr = true;
+                                     static_cast<int>(kLowSmem)));
+        QC_CUDA(cudaFuncSetAttribute(k_pass_high, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kHighSmem)));
     }
     int launches = 0;
-    const unsigned low_grid = static_cast<unsigned>(n_slots) << (Q - 12);
-    const unsigned high_grid = static_cast<unsigned>(n_slots) << (Q - 11);
+    const uint32_t low_tiles = static_cast<uint32_t>(n_slots) << (Q - 12);
+    const uint32_t high_tiles = static_cast<uint32_t>(n_slots) << (Q - 11);
+    const unsigned low_grid = std::min<uint32_t>(low_tiles, static_cast<uint32_t>(sms));
+    const unsigned high_grid = std::min<uint32_t>((high_tiles + 1) / 2, static_cast<uint32_t>(sms));
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
@@ -553,7 +655,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int active = fa ? n_slots : std::max(nph, nmix);
         const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream);
-        k_pass_low<<<low_grid, kLowThreads, 4096 * 16, stream>>>(d_slots, d_lp, l, Q, fa);
+        k_pass_low<<<low_grid, kLowThreads, kLowSmem, stream>>>(d_slots, d_lp, l, Q, fa, low_tiles);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -567,24 +669,29 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             else
                 bh = nmix * 32.0 * N;
             if (prof) prof->begin(K_PASS_HIGH, bh, stream);
-            k_pass_high<<<high_grid, kHighThreads, 0, stream>>>(d_slots, d_lp, l, Q, plan.high[h],
-                                                                fh);
+            k_pass_high<<<high_grid, kHighThreads, kHighSmem, stream>>>(d_slots, d_lp, l, Q,
+                                                                        plan.high[h], fh,
+                                                                        high_tiles);
             if (prof) prof->end(stream);
             ++launches;
         }
     }
     QC_CUDA(cudaGetLastError());
     if (flags & F_EXPECT) {
-        const int chains = static_cast<int>(partials_per_slot(plan));
-        const int total = chains * n_slots;
+        const int nbl = 1 << (Q - 12);
+        const int warps = nbl * n_slots;
+        const size_t smem = static_cast<size_t>(kSumWarps) * 2 * 2 * kSumChunk * sizeof(double);
+        static bool sum_attr = false;
+        if (!sum_attr) {
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            sum_attr = true;
+        }
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream);
-        k_blocksum<<<(total + kSumThreads - 1) / kSumThreads, kSumThreads, 0, stream>>>(
-            d_slots, n_slots, Q, plan.sym ? 1 : 0, d_partials);
+        k_blocksum<<<(warps + kSumWarps - 1) / kSumWarps, kSumWarps * 32, smem, stream>>>(
+            d_slots, n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
-        if (prof) prof->begin(K_FINALSUM, static_cast<double>(total) * 8.0, stream);
-        k_finalsum<<<(n_slots + 63) / 64, 64, 0, stream>>>(d_partials, n_slots, chains, d_out);
-        if (prof) prof->end(stream);
-        launches += 2;
+        launches += 1;
         QC_CUDA(cudaGetLastError());
     }
     return launches;
