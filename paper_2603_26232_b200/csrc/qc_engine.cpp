@@ -277,6 +277,8 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             stats.phase[static_cast<size_t>(l)] += L.phase;
             stats.mix[static_cast<size_t>(l)] += L.mix;
             L.lut = nullptr;
+            L.lut_len = 0;
+            L.pad = 0;
             if (L.phase && dgk.integral && !dgk.unit_cost) {
                 // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c)
                 double* dst = hlut + 2 * lut_pos;
@@ -286,6 +288,7 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
                     dst[2 * c + 1] = z.imag();
                 }
                 L.lut = reinterpret_cast<const double2*>(d + o_lut) + lut_pos;
+                L.lut_len = dgk.lut_len;
                 lut_pos += static_cast<size_t>(dgk.lut_len);
             }
         }

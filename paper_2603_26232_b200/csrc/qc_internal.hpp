@@ -50,6 +50,8 @@ struct LayerParam {
     double c, s;           // cos(beta), sin(beta) (host libm, statevector.hpp:192)
     int32_t phase;         // gamma != 0 (statevector.hpp:149)
     int32_t mix;           // !(s == 0 && c == 1) (statevector.hpp:193)
+    int32_t lut_len;       // entries of lut
+    int32_t pad;
 };
 
 // Mode flags for a launch chain.
@@ -60,11 +62,13 @@ enum : uint32_t {
     F_SYM = 8u,         // half-state storage (complement symmetry), else full state
 };
 
-// One high (gather) pass: 3 column bits (0,1,2) + 8 tile bits.
+// One high (gather) pass: 3 column bits (0,1,2) + kHighBits tile bits.
+constexpr int kHighBits = 9;
 struct HighPass {
-    uint32_t mask[8];   // tile bit masks (single bit, or ALL for the mirror pseudo-bit)
-    int32_t kind[8];    // 0 batch (no op), 1 RX target, 2 mirror (target q-1 in SYM mode)
-    uint32_t freemask;  // stored-index bits enumerated by the tile index
+    uint32_t mask[kHighBits];  // tile bit masks (single bit, or ALL for the mirror pseudo-bit)
+    int32_t kind[kHighBits];   // 0 batch (no op), 1 RX target, 2 mirror (RX on qubit q-1)
+    uint32_t freemask;         // stored-index bits enumerated by the tile index
+    int32_t mpos;              // tile-bit index of the mirror pseudo-bit, -1 if none
 };
 
 struct ChainPlan {

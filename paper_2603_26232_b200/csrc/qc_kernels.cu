@@ -18,7 +18,7 @@
 //
 // Passes (Q > 12), one HBM round trip each:
 //   pass A  (k_pass_low):  2^12 contiguous amps per CTA, [init |+>] + phase + RX 0..11
-//   pass Bk (k_pass_high): 8 gather bits x 8-amp columns per CTA, RX on bits >= 12,
+//   pass Bk (k_pass_high): 9 gather bits x 8-amp columns per CTA, RX on bits >= 12,
 //                          mirror op last; the final one emits f(z)=|a|^2 C(z)
 //   k_blocksum: the blocked sequential expectation over f (+ the in-order block sum).
 // Q <= 12 (k_onchip): the whole state lives in one CTA's shared memory for all layers.
@@ -221,150 +221,140 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const SlotDesc* __res
 }
 
 // ---------------------------------------------------------------------------
-// cp.async (LDGSTS) helpers: 16-byte global->shared copies that bypass registers, so a
-// persistent CTA streams its next tile in while it computes the current one.
+// Pass kernels: 512 threads x 8 amplitudes per 4096-amp tile, rounds of 3 targets in
+// registers exchanged through shared memory. 8 amps/thread keeps registers <= 64 so
+// two CTAs (32 warps) share an SM and one CTA's global loads overlap the other's FP64
+// rounds. Shared layout: e ^ ((e >> 3) & 7) (the 128-byte XOR swizzle) is
+// conflict-free for every round's 16-byte accesses.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void bar_named(int id, int n) {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
-}
+constexpr int kPassThreads = 512;
+constexpr int kLutSmem = 512;  // LUT entries staged in shared memory (else read from L1/L2)
+constexpr size_t kPassSmem = 4096 * sizeof(double2) + kLutSmem * sizeof(double2);
 
-// ---------------------------------------------------------------------------
-// k_pass_low: pass A, 4096 contiguous stored amplitudes per tile, targets 0..11.
-// Persistent: one 256-thread CTA per SM walks tiles blockIdx.x, +gridDim.x, ...;
-// tile k+1 (amplitudes + cut levels) is prefetched with cp.async into the other
-// stage while tile k runs three register rounds of 4 targets (16 amps/thread)
-// exchanged through an XOR-swizzled stage (conflict-free 16-byte accesses).
-// ---------------------------------------------------------------------------
-constexpr int kLowThreads = 256;
-constexpr size_t kLowSmem = 2 * 4096 * sizeof(double2) + 2 * 4096 * sizeof(uint16_t);
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 3) & 7u); }
 
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 4) & 7u); }
-
-// Apply RX on the 4 thread-local bits (ascending) of a[16].
-__device__ __forceinline__ void rx_local4(double2 (&a)[16], double c, double s) {
+// RX on the 3 thread-local bits (ascending) of a[8].
+__device__ __forceinline__ void rx_local3(double2 (&a)[8], double c, double s) {
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 3; ++b) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < 8; ++j)
             if (!(j & (1 << b))) rx_rn(a[j], a[j | (1 << b)], c, s);
     }
 }
 
-__global__ void __launch_bounds__(kLowThreads, 1) k_pass_low(const SlotDesc* __restrict__ slots,
-                                                           const LayerParam* __restrict__ lp,
-                                                           int layer, int Q, uint32_t flags,
-                                                           uint32_t total_tiles) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double2* buf = reinterpret_cast<double2*>(smraw);                       // [2][4096]
-    uint16_t* levs = reinterpret_cast<uint16_t*>(smraw + 2 * 4096 * sizeof(double2));  // [2][4096]
+// k_pass_low: pass A, tile = 4096 contiguous stored amplitudes, targets 0..11
+// (rounds: bits 0-2, 3-5, 6-8, 9-11), [|+> init] + phase first.
+__global__ void __launch_bounds__(kPassThreads, 2) k_pass_low(const SlotDesc* __restrict__ slots,
+                                                            const LayerParam* __restrict__ lp,
+                                                            int layer, int Q, uint32_t flags) {
+    extern __shared__ __align__(16) double2 sm[];
+    double2* slut = sm + 4096;
     const int tshift = Q - 12;
-    const uint32_t tmask = (1u << tshift) - 1u;
+    const int slot = blockIdx.x >> tshift;
+    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
+    const SlotDesc S = slots[slot];
+    const LayerParam L = lp[S.layer_base + layer];
     const bool init = flags & F_INIT;
+    if (!init && !L.phase && !L.mix) return;  // identity layer: memory already holds it
+    const uint32_t base = tile << 12;
+    double2* __restrict__ st = S.state + base;
     const uint32_t tid = threadIdx.x;
-
-    auto issue = [&](uint32_t t, int stage) {
-        if (t < total_tiles) {
-            const SlotDesc& S = slots[t >> tshift];
-            const LayerParam& L = lp[S.layer_base + layer];
-            if (init || L.phase || L.mix) {
-                const uint32_t base = (t & tmask) << 12;
-                if (!init) {
-                    const double2* src = S.state + base;
-                    double2* dst = buf + stage * 4096;
+    double2 a[8];
+    // issue every global load up front: amplitudes (coalesced), levels (one 16-byte
+    // vector per thread, the 8 levels of its round-0 amplitudes), LUT -> shared
+    if (!init) {
 #pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        cp_async16(dst + swz(k * kLowThreads + tid), src + k * kLowThreads + tid);
-                }
-                if (L.phase && S.lev) {
-                    const uint16_t* src = S.lev + base;
-                    uint16_t* dst = levs + stage * 4096;
-                    cp_async16(dst + tid * 8, src + tid * 8);
-                    cp_async16(dst + (tid + 256) * 8, src + (tid + 256) * 8);
-                }
-            }
-        }
-        cp_commit();
-    };
-
-    uint32_t t = blockIdx.x;
-    issue(t, 0);
-    for (int k = 0; t < total_tiles; ++k, t += gridDim.x) {
-        const int stage = k & 1;
-        issue(t + gridDim.x, stage ^ 1);
-        cp_wait1();
-        __syncthreads();
-        const SlotDesc S = slots[t >> tshift];
-        const LayerParam L = lp[S.layer_base + layer];
-        if (init || L.phase || L.mix) {  // else: identity layer, memory already holds it
-            const uint32_t base = (t & tmask) << 12;
-            double2* sm = buf + stage * 4096;
-            const uint16_t* lv = levs + stage * 4096;
-            double2 a[16];
-            // round 0: bits 0..3 thread-local (e = tid*16 + j), phase first
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t e = tid * 16u + j;
-                double2 v = init ? make_double2(S.amp0, 0.0) : sm[swz(e)];
-                if (L.phase) {
-                    if (S.lev)
-                        v = cmul_rn(v, L.lut[lv[e]]);
-                    else
-                        v = phase_rn(v, S, L, base + e);
-                }
-                a[j] = v;
-            }
-            if (L.mix) rx_local4(a, L.c, L.s);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sm[swz(tid * 16u + j)] = a[j];
-            __syncthreads();
-            // round 1: bits 4..7 (e = (tid>>4)<<8 | j<<4 | tid&15)
-            const uint32_t r1 = ((tid >> 4) << 8) | (tid & 15u);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) a[j] = sm[swz(r1 | (j << 4))];
-            if (L.mix) rx_local4(a, L.c, L.s);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) sm[swz(r1 | (j << 4))] = a[j];
-            __syncthreads();
-            // round 2: bits 8..11 (e = j<<8 | tid), stored straight back (coalesced)
-#pragma unroll
-            for (int j = 0; j < 16; ++j) a[j] = sm[swz((j << 8) | tid)];
-            if (L.mix) rx_local4(a, L.c, L.s);
-            double2* st = S.state + base;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) st[(j << 8) | tid] = a[j];
-        }
-        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+        for (int k = 0; k < 8; ++k) a[k] = st[k * kPassThreads + tid];
     }
+    const bool use_lev = L.phase && S.lev;
+    uint4 lv4 = make_uint4(0, 0, 0, 0);
+    if (use_lev) lv4 = *reinterpret_cast<const uint4*>(S.lev + base + tid * 8u);
+    const bool lut_sm = use_lev && L.lut_len <= kLutSmem;
+    if (lut_sm)
+        for (int i = tid; i < L.lut_len; i += kPassThreads) slut[i] = L.lut[i];
+    if (!init) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sm[swz(k * kPassThreads + tid)] = a[k];
+    }
+    __syncthreads();
+    // round 0: bits 0..2 (e = tid*8 + j), phase first
+    {
+        const uint32_t lvw[4] = {lv4.x, lv4.y, lv4.z, lv4.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t e = tid * 8u + j;
+            double2 v = init ? make_double2(S.amp0, 0.0) : sm[swz(e)];
+            if (L.phase) {
+                if (use_lev) {
+                    const uint32_t lev = (lvw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+                    v = cmul_rn(v, lut_sm ? slut[lev] : L.lut[lev]);
+                } else {
+                    v = phase_rn(v, S, L, base + e);
+                }
+            }
+            a[j] = v;
+        }
+        if (L.mix) rx_local3(a, L.c, L.s);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm[swz(tid * 8u + j)] = a[j];
+    }
+    __syncthreads();
+    // round 1: bits 3..5 (e = (tid>>3)<<6 | j<<3 | tid&7)
+    {
+        const uint32_t r = ((tid >> 3) << 6) | (tid & 7u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 3))];
+        if (L.mix) rx_local3(a, L.c, L.s);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm[swz(r | (j << 3))] = a[j];
+    }
+    __syncthreads();
+    // round 2: bits 6..8 (e = (tid>>6)<<9 | j<<6 | tid&63)
+    {
+        const uint32_t r = ((tid >> 6) << 9) | (tid & 63u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 6))];
+        if (L.mix) rx_local3(a, L.c, L.s);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm[swz(r | (j << 6))] = a[j];
+    }
+    __syncthreads();
+    // round 3: bits 9..11 (e = j<<9 | tid), stored straight back (coalesced)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = sm[swz((j << 9) | tid)];
+    if (L.mix) rx_local3(a, L.c, L.s);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) st[(j << 9) | tid] = a[j];
 }
 
 // ---------------------------------------------------------------------------
-// k_pass_high: 3 column bits (8 contiguous amps) x 8 tile bits per tile.
+// k_pass_high: 3 column bits (8 contiguous amps, bits 0..2) x 9 tile bits per tile.
 // Tile bit kinds: 1 RX target (mask = one stored bit), 2 mirror (mask = all Q bits,
 // RX on qubit q-1), 0 batch (no op). Targets precede the mirror in tile-bit order.
 // In the mirror half of a tile (mirror bit set) every stored bit is complemented, so
-// the RX roles (a0 = bit clear) of target pairs swap.
-// Persistent: each 256-thread CTA runs two independent 128-thread tile streams
-// (named barriers), each double-buffering its next tile's 128-byte column segments
-// with cp.async.
+// the RX roles (a0 = bit clear) of target pairs swap. Rounds: tile bits 0-2, 3-5, 6-8;
+// shared index e = w | tilebits << 3 (lanes vary w: conflict-free without swizzle).
 // ---------------------------------------------------------------------------
-constexpr int kHighThreads = 256;
-constexpr size_t kHighSmem = 2 * 2 * 2048 * sizeof(double2);
+__device__ __forceinline__ uint32_t tile_xor(const HighPass& hp, uint32_t bits) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < kHighBits; ++b)
+        if ((bits >> b) & 1u) x ^= hp.mask[b];
+    return x;
+}
 
 template <int OFF>
-__device__ __forceinline__ void high_round(double2 (&a)[16], const HighPass& hp, int mir_local,
-                                           bool mir_thread, double c, double s) {
+__device__ __forceinline__ void high_round(double2 (&a)[8], const HighPass& hp, bool mir_thread,
+                                           double c, double s) {
+    constexpr int kNoLocal = -1;
+    const int mir_local = (hp.mpos >= OFF && hp.mpos < OFF + 3) ? hp.mpos - OFF : kNoLocal;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < 3; ++b) {
         const int kind = hp.kind[OFF + b];
         if (kind == 0) continue;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < 8; ++j) {
             if (j & (1 << b)) continue;
             if (kind == 2) {
                 rx_rn(a[j], a[j | (1 << b)], c, s);  // mirror: role order is immaterial
@@ -379,95 +369,72 @@ __device__ __forceinline__ void high_round(double2 (&a)[16], const HighPass& hp,
     }
 }
 
-__global__ void __launch_bounds__(kHighThreads, 1) k_pass_high(const SlotDesc* __restrict__ slots,
+__global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* __restrict__ slots,
                                                              const LayerParam* __restrict__ lp,
                                                              int layer, int Q, HighPass hp,
-                                                             uint32_t flags, uint32_t total_tiles) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    const int half = threadIdx.x >> 7;
-    double2* hbuf = reinterpret_cast<double2*>(smraw) + half * 2 * 2048;  // [2][2048]
-    const int tshift = Q - 11;
-    const uint32_t tmask = (1u << tshift) - 1u;
+                                                             uint32_t flags) {
+    extern __shared__ __align__(16) double2 sm[];
+    const int tshift = Q - 12;
+    const int slot = blockIdx.x >> tshift;
+    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
+    const SlotDesc S = slots[slot];
+    const LayerParam L = lp[S.layer_base + layer];
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
-    const uint32_t ht = threadIdx.x & 127u;
-    const uint32_t w = ht & 7u;
-    const uint32_t hb = ht >> 3;  // round 0: tile bits 4..7; round 1: tile bits 0..3
-    int mpos = -1;                // tile-bit index of the mirror pseudo-bit
+    if (!L.mix && !fout) return;
+    const bool mix = L.mix;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t w = tid & 7u;
+    const uint32_t tb = tid >> 3;  // 6 tile bits held by the thread
+    const uint32_t x = deposit(tile, hp.freemask) | w;
+    const int mp = hp.mpos;
+    auto mbit = [&](uint32_t tilebits) { return mp >= 0 && ((tilebits >> mp) & 1u); };
+    double2 a[8];
+    // output addresses of round 2 (tile bits 0-5 = tb, 6-8 = j) and their levels, early
+    const uint32_t g2 = x ^ tile_xor(hp, tb);
+    uint32_t lv[8];
+    if (fout) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (hp.kind[k] == 2) mpos = k;
-    // XOR of the thread's own tile-bit masks
-    uint32_t thr_hi = 0, thr_lo = 0;
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        if ((hb >> b) & 1u) thr_hi ^= hp.mask[4 + b];
-        if ((hb >> b) & 1u) thr_lo ^= hp.mask[b];
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
+            lv[j] = S.lev ? S.lev[g] : 0u;
+        }
     }
-    const uint32_t streams = 2 * gridDim.x;
-
-    auto issue = [&](uint32_t t, int stage) {
-        if (t < total_tiles) {
-            const SlotDesc& S = slots[t >> tshift];
-            const LayerParam& L = lp[S.layer_base + layer];
-            if (L.mix || fout) {
-                const uint32_t gt = deposit(t & tmask, hp.freemask) | w;
-                double2* dst = hbuf + stage * 2048;
+    // round 0: tile bits 0-2 local, thread holds tile bits 3-8 = tb (coalesced by w)
+    {
+        const uint32_t tbits = tb << 3;
+        const uint32_t g0 = x ^ tile_xor(hp, tbits);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    uint32_t g = gt ^ thr_hi;
+        for (int j = 0; j < 8; ++j) a[j] = S.state[g0 ^ tile_xor(hp, static_cast<uint32_t>(j))];
+        if (mix) high_round<0>(a, hp, mbit(tbits), L.c, L.s);
 #pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        if ((j >> b) & 1) g ^= hp.mask[b];
-                    cp_async16(dst + (w | (j << 3) | (hb << 7)), S.state + g);
-                }
-            }
+        for (int j = 0; j < 8; ++j) sm[w | (j << 3) | (tb << 6)] = a[j];
+    }
+    __syncthreads();
+    // round 1: tile bits 3-5 local, thread holds tile bits 0-2 and 6-8
+    {
+        const uint32_t tbits = (tb & 7u) | ((tb >> 3) << 6);
+        const uint32_t e0 = w | ((tb & 7u) << 3) | ((tb >> 3) << 9);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = sm[e0 | (j << 6)];
+        if (mix) high_round<3>(a, hp, mbit(tbits), L.c, L.s);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm[e0 | (j << 6)] = a[j];
+    }
+    __syncthreads();
+    // round 2: tile bits 6-8 local, thread holds tile bits 0-5 = tb
+    {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] = sm[w | (tb << 3) | (j << 9)];
+        if (mix) high_round<6>(a, hp, mbit(tb), L.c, L.s);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
+            if (sout) S.state[g] = a[j];
+            if (fout)
+                S.fbuf[g] = __dmul_rn(norm_rn(a[j]),
+                                      S.lev ? static_cast<double>(lv[j]) : (S.val ? S.val[g] : 1.0));
         }
-        cp_commit();
-    };
-
-    uint32_t t = blockIdx.x * 2 + half;
-    issue(t, 0);
-    for (int k = 0; t < total_tiles; ++k, t += streams) {
-        const int stage = k & 1;
-        issue(t + streams, stage ^ 1);
-        cp_wait1();
-        const SlotDesc S = slots[t >> tshift];
-        const LayerParam L = lp[S.layer_base + layer];
-        if (L.mix || fout) {
-            const bool mix = L.mix;
-            const uint32_t gt = deposit(t & tmask, hp.freemask) | w;
-            double2* sm = hbuf + stage * 2048;
-            double2 a[16];
-            // round 0: tile bits 0..3 local; the thread reads exactly what it copied
-            {
-                const bool mir_t = mpos >= 4 && ((hb >> (mpos - 4)) & 1u);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) a[j] = sm[w | (j << 3) | (hb << 7)];
-                if (mix) high_round<0>(a, hp, mpos < 4 ? mpos : -1, mir_t, L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) sm[w | (j << 3) | (hb << 7)] = a[j];
-            }
-            bar_named(1 + half, 128);
-            // round 1: tile bits 4..7 local; thread = (w, tile bits 0..3 = hb)
-            {
-                const bool mir_t = mpos >= 0 && mpos < 4 && ((hb >> mpos) & 1u);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) a[j] = sm[w | (hb << 3) | (j << 7)];
-                if (mix) high_round<4>(a, hp, mpos >= 4 ? mpos - 4 : -1, mir_t, L.c, L.s);
-                const uint32_t g0 = gt ^ thr_lo;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    uint32_t g = g0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        if ((j >> b) & 1) g ^= hp.mask[4 + b];
-                    if (sout) S.state[g] = a[j];
-                    if (fout) S.fbuf[g] = __dmul_rn(norm_rn(a[j]), cost_of(S, g));
-                }
-            }
-        }
-        bar_named(1 + half, 128);  // this stage is refilled by the next prefetch
     }
 }
 
@@ -564,16 +531,18 @@ ChainPlan plan_chain(int q, bool sym) {
     for (int b = 12; b < Q; ++b) items.push_back(b);
     if (sym) items.push_back(-1);
     const uint32_t all = (Q == 32) ? ~0u : ((1u << Q) - 1u);
-    for (size_t i = 0; i < items.size(); i += 8) {
+    for (size_t i = 0; i < items.size(); i += kHighBits) {
         HighPass hp{};
+        hp.mpos = -1;
         uint32_t single = 0x7u;  // column bits 0..2
         bool mirror = false;
         int k = 0;
-        for (; k < 8 && i + k < items.size(); ++k) {
+        for (; k < kHighBits && i + k < items.size(); ++k) {
             const int it = items[i + k];
             if (it < 0) {
                 hp.mask[k] = all;
                 hp.kind[k] = 2;
+                hp.mpos = k;
                 mirror = true;
             } else {
                 hp.mask[k] = 1u << it;
@@ -581,7 +550,7 @@ ChainPlan plan_chain(int q, bool sym) {
                 single |= 1u << it;
             }
         }
-        for (int pad = 3; k < 8; ++pad) {  // batch bits: widen the contiguous columns
+        for (int pad = 3; k < kHighBits; ++pad) {  // batch bits: widen the contiguous columns
             hp.mask[k] = 1u << pad;
             hp.kind[k] = 0;
             single |= 1u << pad;
@@ -632,21 +601,16 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         QC_CUDA(cudaGetLastError());
         return 1;
     }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QC_CUDA(cudaGetDevice(&dev));
-        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static bool attrs = false;
+    if (!attrs) {
         QC_CUDA(cudaFuncSetAttribute(k_pass_low, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kLowSmem)));
+                                     static_cast<int>(kPassSmem)));
         QC_CUDA(cudaFuncSetAttribute(k_pass_high, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kHighSmem)));
+                                     static_cast<int>(4096 * sizeof(double2))));
+        attrs = true;
     }
     int launches = 0;
-    const uint32_t low_tiles = static_cast<uint32_t>(n_slots) << (Q - 12);
-    const uint32_t high_tiles = static_cast<uint32_t>(n_slots) << (Q - 11);
-    const unsigned low_grid = std::min<uint32_t>(low_tiles, static_cast<uint32_t>(sms));
-    const unsigned high_grid = std::min<uint32_t>((high_tiles + 1) / 2, static_cast<uint32_t>(sms));
+    const unsigned grid = static_cast<unsigned>(n_slots) << (Q - 12);
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
@@ -655,7 +619,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int active = fa ? n_slots : std::max(nph, nmix);
         const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream);
-        k_pass_low<<<low_grid, kLowThreads, kLowSmem, stream>>>(d_slots, d_lp, l, Q, fa, low_tiles);
+        k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -669,9 +633,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             else
                 bh = nmix * 32.0 * N;
             if (prof) prof->begin(K_PASS_HIGH, bh, stream);
-            k_pass_high<<<high_grid, kHighThreads, kHighSmem, stream>>>(d_slots, d_lp, l, Q,
-                                                                        plan.high[h], fh,
-                                                                        high_tiles);
+            k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
+                d_slots, d_lp, l, Q, plan.high[h], fh);
             if (prof) prof->end(stream);
             ++launches;
         }
