@@ -104,12 +104,12 @@ using namespace qcg;
 // ---------------------------------------------------------------------------
 // engine
 // ---------------------------------------------------------------------------
-void qc_engine::h2d_copy(void* dst, const void* src, size_t bytes) {
-    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+void qc_engine::h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st ? st : stream));
     h2d += bytes;
 }
-void qc_engine::d2h_copy(void* dst, const void* src, size_t bytes) {
-    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+void qc_engine::d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    QC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st ? st : stream));
     d2h += bytes;
 }
 
@@ -193,12 +193,13 @@ size_t qc_engine::chunk_slots(int Q, bool onchip, size_t n) const {
         const long v = std::strtol(env, nullptr, 10);
         if (v > 0) return std::min<size_t>(n, static_cast<size_t>(v));
     }
-    if (onchip) return std::max<size_t>(1, (n + 1) / 2);  // two chunks: host/device overlap
-    const size_t per = (size_t{1} << Q) * 26;              // state 16 + f 8 + levels 2 B/amp
-    const size_t l2_target = size_t{96} << 20;              // of the 126 MB L2
-    size_t g = std::max<size_t>(1, l2_target / per);
-    const size_t chunks = (n + g - 1) / g;
-    return (n + chunks - 1) / chunks;                        // balance the chunks
+    // Two chunks on two streams: while one chunk's NM step is prepared on the host the
+    // other chunk's kernels run, and the two chunks' grids fill each other's tails.
+    // (Single-stream L2-sized chunks of 4-11 slots measured slower on B200: 134-241 ms vs
+    // 122 ms per C2 solve in one chunk.)
+    if (const char* env = std::getenv("QCG_STREAMS"))
+        if (std::strtol(env, nullptr, 10) == 1) return onchip ? std::max<size_t>(1, (n + 1) / 2) : n;
+    return std::max<size_t>(1, (n + 1) / 2);
 }
 
 void qc_engine::reserve(int Q, bool need_fbuf, size_t slots) {
@@ -219,6 +220,7 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     ctx.n = n;
     ctx.flags = flags;
     if (n <= 0) return;
+    cudaStream_t cs = ctx.st ? ctx.st : stream;
     const DevGraph& g0 = dg[static_cast<size_t>(pts[0].g)];
     const ChainPlan plan = plan_chain(g0.q, g0.sym);
     const size_t N = size_t{1} << plan.Q;
@@ -293,16 +295,16 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             }
         }
     }
-    h2d_copy(d, h, bytes);
+    h2d_copy(d, h, bytes, cs);
     launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
                              reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, part,
-                             tick, od, stream, &stats, &prof);
+                             tick, od, cs, &stats, &prof);
     if (flags & F_EXPECT) {
         auto* ho = static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8));
-        d2h_copy(ho, od, static_cast<size_t>(n) * 8);
+        d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
     }
     if (!ctx.done) QC_CUDA(cudaEventCreateWithFlags(&ctx.done, cudaEventDisableTiming));
-    QC_CUDA(cudaEventRecord(ctx.done, stream));
+    QC_CUDA(cudaEventRecord(ctx.done, cs));
 }
 
 void qc_engine::wait_chunk(ChunkCtx& ctx, double* out) {
@@ -377,6 +379,13 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             const size_t nchunks = (ns + per - 1) / per;
             e->reserve(plan.Q, !plan.onchip, ns);
             std::vector<ChunkCtx> ctx(nchunks);
+            // the aux stream must see the cut tables / zeroed tickets written on the main one
+            cudaEvent_t ready;
+            QC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            QC_CUDA(cudaEventRecord(ready, e->stream));
+            QC_CUDA(cudaStreamWaitEvent(e->aux, ready, 0));
+            QC_CUDA(cudaEventDestroy(ready));
+            for (size_t c = 0; c < nchunks; ++c) ctx[c].st = (c & 1) ? e->aux : e->stream;
             std::vector<std::vector<EvalPoint>> pts(nchunks);
             std::vector<std::vector<size_t>> who(nchunks);
             std::vector<char> inflight(nchunks, 0);
@@ -593,6 +602,7 @@ int qc_engine_create(int device, qc_engine** out) {
         auto* e = new qc_engine();
         e->device = device;
         QC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        QC_CUDA(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
         *out = e;
     });
 }
@@ -601,7 +611,9 @@ void qc_engine_destroy(qc_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
+    cudaStreamSynchronize(e->aux);
     cudaStreamDestroy(e->stream);
+    cudaStreamDestroy(e->aux);
     delete e;
 }
 

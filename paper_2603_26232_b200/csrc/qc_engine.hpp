@@ -61,6 +61,7 @@ struct ChunkCtx {
     int n = 0;
     uint32_t flags = 0;
     double* d_out = nullptr;
+    cudaStream_t st = nullptr;  // stream the chunk runs on (null: the engine stream)
     ChunkCtx() = default;
     ChunkCtx(const ChunkCtx&) = delete;
     ChunkCtx& operator=(const ChunkCtx&) = delete;
@@ -74,6 +75,7 @@ struct ChunkCtx {
 struct qc_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // second stream: alternate chunks overlap on the device
     uint64_t launches = 0;
     uint64_t mem_budget = 0;
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
@@ -85,8 +87,8 @@ struct qc_engine {
     // the engine's shared `tables` buffer, valid until the next prepare()).
     std::vector<qcg::DevGraph> prepare(const std::vector<qcg::HostGraph>& hg, bool allow_sym,
                                        bool unit_cost = false, qcg::DevBuf* target = nullptr);
-    void h2d_copy(void* dst, const void* src, size_t bytes);
-    void d2h_copy(void* dst, const void* src, size_t bytes);
+    void h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t st = nullptr);
+    void d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t st = nullptr);
     // Evaluate points sharing (q, p) in chunks; out[k] = <C> of point k.
     // flags: qcg::F_* (F_STATE_OUT keeps each chunk's states for `on_chunk`).
     size_t max_slots(int Q, bool onchip) const;

@@ -486,15 +486,39 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __r
     stash(0);
     __syncwarp();
     double acc = 0.0;
+    // lanes 0 and 1 run the two chains in lockstep (no divergence): lane 0 ascending over
+    // the block's own chunk, lane 1 descending over the mirror chunk; values are read as
+    // 16-byte pairs ahead of the dependent adds.
+    const bool desc = lane == 1;
     for (int c = 0; c < kChunks; ++c) {
         if (c + 1 < kChunks) load(c + 1);  // in flight while the chains run
-        const double* cur = wb + (c & 1) * 2 * kSumChunk;
-        if (lane == 0) {
-#pragma unroll 16
-            for (int k = 0; k < kSumChunk; ++k) acc = __dadd_rn(acc, cur[k]);
-        } else if (lane == 1 && sym) {
-#pragma unroll 16
-            for (int k = kSumChunk - 1; k >= 0; --k) acc = __dadd_rn(acc, cur[kSumChunk + k]);
+        const double2* cur = reinterpret_cast<const double2*>(wb + (c & 1) * 2 * kSumChunk +
+                                                               (desc ? kSumChunk : 0));
+        if (lane < 2) {
+            // software pipeline: the adds of group g use registers loaded one group earlier
+            auto fetch = [&](int g, double2 (&v)[8]) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    v[u] = cur[desc ? (kSumChunk / 2 - 1 - (8 * g + u)) : (8 * g + u)];
+            };
+            double2 va[8], vb[8];
+            fetch(0, va);
+            constexpr int kGroups = kSumChunk / 16;
+#pragma unroll 1
+            for (int g = 0; g < kGroups; g += 2) {
+                fetch(g + 1, vb);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __dadd_rn(acc, desc ? va[u].y : va[u].x);
+                    acc = __dadd_rn(acc, desc ? va[u].x : va[u].y);
+                }
+                if (g + 2 < kGroups) fetch(g + 2, va);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __dadd_rn(acc, desc ? vb[u].y : vb[u].x);
+                    acc = __dadd_rn(acc, desc ? vb[u].x : vb[u].y);
+                }
+            }
         }
         __syncwarp();
         if (c + 1 < kChunks) stash((c + 1) & 1);
