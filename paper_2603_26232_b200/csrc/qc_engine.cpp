@@ -193,13 +193,15 @@ size_t qc_engine::chunk_slots(int Q, bool onchip, size_t n) const {
         const long v = std::strtol(env, nullptr, 10);
         if (v > 0) return std::min<size_t>(n, static_cast<size_t>(v));
     }
-    // Two chunks on two streams: while one chunk's NM step is prepared on the host the
-    // other chunk's kernels run, and the two chunks' grids fill each other's tails.
-    // (Single-stream L2-sized chunks of 4-11 slots measured slower on B200: 134-241 ms vs
-    // 122 ms per C2 solve in one chunk.)
-    if (const char* env = std::getenv("QCG_STREAMS"))
-        if (std::strtol(env, nullptr, 10) == 1) return onchip ? std::max<size_t>(1, (n + 1) / 2) : n;
-    return std::max<size_t>(1, (n + 1) / 2);
+    // Chunks on separate streams: while one chunk's NM step is prepared on the host the
+    // other chunks' kernels run, and their grids fill each other's tails; one chunk's
+    // latency-bound expectation chains overlap another's passes. (Single-stream
+    // L2-sized chunks of 4-11 slots measured slower on B200: 134-241 ms vs 122 ms per C2
+    // solve in one chunk; two chunks on two streams: 108.5 ms.)
+    size_t chunks = 2;
+    if (const char* env = std::getenv("QCG_CHUNKS")) chunks = std::max(1L, std::strtol(env, nullptr, 10));
+    chunks = std::min(chunks, n);
+    return std::max<size_t>(1, (n + chunks - 1) / chunks);
 }
 
 void qc_engine::reserve(int Q, bool need_fbuf, size_t slots) {
@@ -383,9 +385,13 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             cudaEvent_t ready;
             QC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
             QC_CUDA(cudaEventRecord(ready, e->stream));
-            QC_CUDA(cudaStreamWaitEvent(e->aux, ready, 0));
+            size_t nstreams = 4;
+            if (const char* env = std::getenv("QCG_STREAMS"))
+                nstreams = static_cast<size_t>(std::min(4L, std::max(1L, std::strtol(env, nullptr, 10))));
+            for (size_t k = 0; k + 1 < nstreams; ++k) QC_CUDA(cudaStreamWaitEvent(e->aux[k], ready, 0));
             QC_CUDA(cudaEventDestroy(ready));
-            for (size_t c = 0; c < nchunks; ++c) ctx[c].st = (c & 1) ? e->aux : e->stream;
+            for (size_t c = 0; c < nchunks; ++c)
+                ctx[c].st = (c % nstreams) ? e->aux[c % nstreams - 1] : e->stream;
             std::vector<std::vector<EvalPoint>> pts(nchunks);
             std::vector<std::vector<size_t>> who(nchunks);
             std::vector<char> inflight(nchunks, 0);
@@ -602,7 +608,7 @@ int qc_engine_create(int device, qc_engine** out) {
         auto* e = new qc_engine();
         e->device = device;
         QC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-        QC_CUDA(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
+        for (auto& a : e->aux) QC_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
         *out = e;
     });
 }
@@ -611,9 +617,11 @@ void qc_engine_destroy(qc_engine* e) {
     if (!e) return;
     cudaSetDevice(e->device);
     cudaStreamSynchronize(e->stream);
-    cudaStreamSynchronize(e->aux);
+    for (auto a : e->aux) {
+        cudaStreamSynchronize(a);
+        cudaStreamDestroy(a);
+    }
     cudaStreamDestroy(e->stream);
-    cudaStreamDestroy(e->aux);
     delete e;
 }
 

@@ -75,7 +75,7 @@ struct ChunkCtx {
 struct qc_engine {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t aux = nullptr;  // second stream: alternate chunks overlap on the device
+    cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // extra streams: chunks overlap on the device
     uint64_t launches = 0;
     uint64_t mem_budget = 0;
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;

@@ -478,9 +478,10 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __r
         double2* d = reinterpret_cast<double2*>(wb + stage * 2 * kSumChunk);
 #pragma unroll
         for (int u = 0; u < kPer; ++u) d[u * 32 + lane] = rf[u];
-        if (sym)
+        if (sym)  // mirror chunk stored reversed: both chains then read ascending
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) d[kSumChunk / 2 + u * 32 + lane] = rb[u];
+            for (int u = 0; u < kPer; ++u)
+                d[kSumChunk / 2 + (kSumChunk / 2 - 1 - (u * 32 + lane))] = make_double2(rb[u].y, rb[u].x);
     };
     load(0);
     stash(0);
@@ -498,8 +499,7 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __r
             // software pipeline: the adds of group g use registers loaded one group earlier
             auto fetch = [&](int g, double2 (&v)[8]) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    v[u] = cur[desc ? (kSumChunk / 2 - 1 - (8 * g + u)) : (8 * g + u)];
+                for (int u = 0; u < 8; ++u) v[u] = cur[8 * g + u];
             };
             double2 va[8], vb[8];
             fetch(0, va);
@@ -509,14 +509,14 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __r
                 fetch(g + 1, vb);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    acc = __dadd_rn(acc, desc ? va[u].y : va[u].x);
-                    acc = __dadd_rn(acc, desc ? va[u].x : va[u].y);
+                    acc = __dadd_rn(acc, va[u].x);
+                    acc = __dadd_rn(acc, va[u].y);
                 }
                 if (g + 2 < kGroups) fetch(g + 2, va);
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    acc = __dadd_rn(acc, desc ? vb[u].y : vb[u].x);
-                    acc = __dadd_rn(acc, desc ? vb[u].x : vb[u].y);
+                    acc = __dadd_rn(acc, vb[u].x);
+                    acc = __dadd_rn(acc, vb[u].y);
                 }
             }
         }

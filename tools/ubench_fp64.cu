@@ -1,0 +1,79 @@
+// Microbenchmark: FP64 dependent latency and throughput on the current GPU (B200).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_fp64 tools/ubench_fp64.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void chain_dadd(double* out, long long* cyc, int n, double x) {
+    double acc = 0.0;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) acc = __dadd_rn(acc, x);
+    long long t1 = clock64();
+    out[0] = acc;
+    cyc[0] = t1 - t0;
+}
+__global__ void chain_dmul(double* out, long long* cyc, int n, double x) {
+    double acc = 1.0;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) acc = __dmul_rn(acc, x);
+    long long t1 = clock64();
+    out[0] = acc;
+    cyc[0] = t1 - t0;
+}
+__global__ void chain_fadd(float* out, long long* cyc, int n, float x) {
+    float acc = 0.0f;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) acc = __fadd_rn(acc, x);
+    long long t1 = clock64();
+    out[0] = acc;
+    cyc[0] = t1 - t0;
+}
+// 8 independent chains per thread: throughput
+__global__ void tput_dadd(double* out, int n, double x) {
+    double a[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(a[k], x);
+    double s = 0;
+    for (int k = 0; k < 8; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+int main() {
+    double* d;
+    float* f;
+    long long* c;
+    cudaMalloc(&d, 1 << 26);
+    cudaMalloc(&f, 64);
+    cudaMalloc(&c, 64);
+    long long cyc;
+    const int n = 1 << 16;
+    chain_dadd<<<1, 1>>>(d, c, n, 1e-3);
+    chain_dadd<<<1, 1>>>(d, c, n, 1e-3);
+    cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+    printf("dependent DADD latency: %.2f cycles\n", double(cyc) / n);
+    chain_dmul<<<1, 1>>>(d, c, n, 1.0000001);
+    cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+    printf("dependent DMUL latency: %.2f cycles\n", double(cyc) / n);
+    chain_fadd<<<1, 1>>>(f, c, n, 1e-3f);
+    cudaMemcpy(&cyc, c, 8, cudaMemcpyDeviceToHost);
+    printf("dependent FADD latency: %.2f cycles\n", double(cyc) / n);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int it = 4096;
+    tput_dadd<<<sms * 8, 256>>>(d, it, 1e-3);
+    cudaEventRecord(e0);
+    tput_dadd<<<sms * 8, 256>>>(d, it, 1e-3);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = double(sms) * 8 * 256 * it * 8;
+    printf("DADD throughput: %.2f Tops/s (%d SMs, clock %d MHz) = %.1f per SM per cycle at max clock\n",
+           ops / ms / 1e9, sms, clk / 1000, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    return 0;
+}
