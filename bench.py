@@ -37,6 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+PROFILE_STRIDE = 16  # per-kernel CUDA events on one launch in 16 (sampled, live)
 METRIC = "end-to-end Max-Cut solve time & subgraph-QAOA evals/s at 1/2/4/8 B200"
 UNIT = "evals/s"
 
@@ -235,34 +236,20 @@ def main():
         def step_value():
             return sess.execute()
     else:
+        from paper_2603_26232_b200.distributed import solve_sharded
         M = eng.subgraph_count(w["n"], edges, **cfg)
-        begin, end = eng.shard_range(M, rank, world)
-        from paper_2603_26232_b200 import kcap_for
-        kcap = kcap_for(w["qubit_cap"], w["top_k"])
-        rb = eng.record_bytes(kcap, w["layers"])
-        maxcount = max(eng.shard_range(M, r, world)[1] - eng.shard_range(M, r, world)[0]
-                       for r in range(world))
 
         def step_value():
-            rec = eng.shard_solve(w["n"], edges, begin, end, rb, **cfg)
-            buf = torch.zeros(maxcount * rb, dtype=torch.uint8, device=f"cuda:{local}")
-            if len(rec):
-                buf[: len(rec)].copy_(torch.from_numpy(rec))
-            out = torch.empty(world * maxcount * rb, dtype=torch.uint8, device=f"cuda:{local}")
-            dist.all_gather_into_tensor(out, buf)  # NCCL over NVLink: the only collective
-            if rank == 0:
-                host = out.cpu().numpy().reshape(world, maxcount * rb)
-                parts = [host[r, : (eng.shard_range(M, r, world)[1] -
-                                    eng.shard_range(M, r, world)[0]) * rb] for r in range(world)]
-                return eng.merge_records(w["n"], edges, np.concatenate(parts), M, **cfg)
-            return None
+            # shard the QAOA stage, one NCCL all-gather of solve records, merge on rank 0
+            return solve_sharded(eng, w["n"], edges, rank, world,
+                                 device=torch.device("cuda", local), **cfg)
 
     def timed(fn, steps, prof=False):
         """per-step device time via CUDA events on the engine stream, L2 flushed between."""
         times, last = [], None
         launches0 = eng.launches
         if prof:
-            eng.profile(True)
+            eng.profile(PROFILE_STRIDE)
         for _ in range(steps):
             flush.zero_()
             barrier()
@@ -337,7 +324,8 @@ def main():
                 "measured" else "fallback (B200_PROFILING.md)",
                 "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
                 "avg_launch_ms": d["ms"] / max(d["launches"], 1),
-                "share_of_step": d["ms"] / 1e3 / (sum(t_val) / 1.0) if sum(t_val) else None,
+                "sampled_launches": d["launches"], "sample_stride": PROFILE_STRIDE,
+                "share_of_step": d["ms"] * PROFILE_STRIDE / 1e3 / sum(t_val) if sum(t_val) else None,
                 "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                 "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
                                 if v["ms"] > 0 else 0.0}

@@ -168,7 +168,7 @@ uint64_t qc_engine_launches(const qc_engine* e);
 /* Device bytes of stored-state / scratch the engine may use; 0 = automatic. */
 int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
 /* Live profiling: with on=1 every engine kernel is bracketed by CUDA events on the
- * engine's stream; qc_engine_profile_read returns, per kernel kind (0 levels, 1 onchip,
+ * stream it runs on (on=N>1: one launch in N per kernel kind is sampled); qc_engine_profile_read returns, per kernel kind (0 levels, 1 onchip,
  * 2 pass_low, 3 pass_high, 4 blocksum, 5 finalsum, 6 topk, 7 merge_tables,
  * 8 merge_search, 9 merge_other), the launch count, summed device ms and summed
  * algorithmic bytes since the last qc_engine_profile call. */

@@ -317,8 +317,9 @@ class Engine:
         self._call("qc_engine_set_memory_budget", C.c_uint64(nbytes))
 
     # ---- instrumentation -----------------------------------------------------------
-    def profile(self, on: bool = True):
-        """Start (and reset) live per-kernel CUDA-event timing on the engine stream."""
+    def profile(self, on: bool | int = True):
+        """Start (and reset) live per-kernel CUDA-event timing; on=N>1 samples one launch
+        in N per kernel kind (keeps the event overhead out of a timed region)."""
         self._call("qc_engine_profile", C.c_int(int(on)))
 
     def profile_read(self) -> dict:
@@ -328,7 +329,7 @@ class Engine:
             ms = C.c_double(0)
             b = C.c_double(0)
             self._call("qc_engine_profile_read", C.c_int(k), C.byref(n), C.byref(ms), C.byref(b))
-            out[name] = dict(launches=int(n.value), ms=ms.value, bytes=b.value)
+            out[name] = dict(launches=int(n.value), ms=ms.value, bytes=b.value)  # sampled
         return out
 
     def transfers(self):

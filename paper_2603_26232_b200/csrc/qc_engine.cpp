@@ -198,7 +198,7 @@ size_t qc_engine::chunk_slots(int Q, bool onchip, size_t n) const {
     // latency-bound expectation chains overlap another's passes. (Single-stream
     // L2-sized chunks of 4-11 slots measured slower on B200: 134-241 ms vs 122 ms per C2
     // solve in one chunk; two chunks on two streams: 108.5 ms.)
-    size_t chunks = 2;
+    size_t chunks = 3;
     if (const char* env = std::getenv("QCG_CHUNKS")) chunks = std::max(1L, std::strtol(env, nullptr, 10));
     chunks = std::min(chunks, n);
     return std::max<size_t>(1, (n + chunks - 1) / chunks);
@@ -385,7 +385,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             cudaEvent_t ready;
             QC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
             QC_CUDA(cudaEventRecord(ready, e->stream));
-            size_t nstreams = 4;
+            size_t nstreams = std::min<size_t>(nchunks, 4);
             if (const char* env = std::getenv("QCG_STREAMS"))
                 nstreams = static_cast<size_t>(std::min(4L, std::max(1L, std::strtol(env, nullptr, 10))));
             for (size_t k = 0; k + 1 < nstreams; ++k) QC_CUDA(cudaStreamWaitEvent(e->aux[k], ready, 0));
@@ -630,6 +630,7 @@ int qc_engine_profile(qc_engine* e, int on) {
         check_engine(e);
         e->prof.reset();
         e->prof.on = on != 0;
+        e->prof.stride = on > 1 ? on : 1;  // on = N > 1: sample one launch in N per kind
     });
 }
 

@@ -89,6 +89,10 @@ enum KernelKind : int {
 };
 struct Prof {
     bool on = false;
+    int stride = 1;  // record one launch in `stride` per kernel kind (sampling keeps the
+                     // event overhead out of the timed region; averages stay per launch)
+    uint64_t seen[K_COUNT] = {};
+    bool open_ = false;
     struct Rec {
         int kind;
         cudaEvent_t a, b;
@@ -110,13 +114,17 @@ struct Prof {
         return e;
     }
     void begin(int kind, double b, cudaStream_t s) {
+        open_ = false;
         if (!on) return;
+        if ((seen[kind]++ % static_cast<uint64_t>(stride)) != 0) return;
         Rec r{kind, ev(), ev(), b};
         cudaEventRecord(r.a, s);
         recs.push_back(r);
+        open_ = true;
     }
     void end(cudaStream_t s) {
-        if (!on || recs.empty()) return;
+        if (!on || !open_ || recs.empty()) return;
+        open_ = false;
         cudaEventRecord(recs.back().b, s);
         if (recs.size() >= 4096) resolve();
     }
@@ -135,7 +143,7 @@ struct Prof {
     }
     void reset() {
         resolve();
-        for (int k = 0; k < K_COUNT; ++k) ms[k] = bytes[k] = 0, count[k] = 0;
+        for (int k = 0; k < K_COUNT; ++k) ms[k] = bytes[k] = 0, count[k] = 0, seen[k] = 0;
     }
     ~Prof() {
         for (auto& r : recs) {

@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
 constexpr int kSumWarps = 4;
-constexpr int kSumChunk = 512;  // doubles per chunk
+constexpr int kSumChunk = 256;  // doubles per chunk (32 KB smem per 4-warp CTA)
 
 __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __restrict__ slots,
                                                           int n_slots, int Q, int sym,
