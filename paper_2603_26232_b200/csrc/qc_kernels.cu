@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 constexpr int kSumWarps = 4;
 constexpr int kSumChunk = 256;  // doubles per chunk (32 KB smem per 4-warp CTA)
 
-__global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __restrict__ slots,
+__global__ void __launch_bounds__(kSumWarps * 32, 4) k_blocksum(const SlotDesc* __restrict__ slots,
                                                           int n_slots, int Q, int sym,
                                                           double* __restrict__ partials,
                                                           unsigned* __restrict__ tickets,
@@ -463,65 +463,78 @@ __global__ void __launch_bounds__(kSumWarps * 32) k_blocksum(const SlotDesc* __r
     if (slot >= n_slots) return;
     const int b = gw - slot * nbl;
     const double2* f2 = reinterpret_cast<const double2*>(slots[slot].fbuf + (size_t)b * kBlock);
-    double* wb = sbuf + (size_t)warp * 2 * 2 * kSumChunk;
+    // per warp: 2 stages x {ascending chunk, pad, mirror chunk (reversed), pad}; the pad
+    // keeps the two chain lanes' 16-byte reads in different banks
+    constexpr int kStage = 2 * kSumChunk + 4;
+    double* wb = sbuf + (size_t)warp * 2 * kStage;
     constexpr int kPer = kSumChunk / 2 / 32;  // double2 per lane per chunk
     constexpr int kChunks = kBlock / kSumChunk;
-    double2 rf[kPer], rb[kPer];
-    auto load = [&](int c) {
+    double2 rf0[kPer], rb0[kPer], rf1[kPer], rb1[kPer];
+    auto load = [&](int c, double2 (&rf)[kPer], double2 (&rb)[kPer]) {
 #pragma unroll
         for (int u = 0; u < kPer; ++u) rf[u] = f2[c * (kSumChunk / 2) + u * 32 + lane];
         if (sym)
 #pragma unroll
             for (int u = 0; u < kPer; ++u) rb[u] = f2[(kChunks - 1 - c) * (kSumChunk / 2) + u * 32 + lane];
     };
-    auto stash = [&](int stage) {
-        double2* d = reinterpret_cast<double2*>(wb + stage * 2 * kSumChunk);
+    auto stash = [&](int stage, const double2 (&rf)[kPer], const double2 (&rb)[kPer]) {
+        double2* d = reinterpret_cast<double2*>(wb + stage * kStage);
 #pragma unroll
         for (int u = 0; u < kPer; ++u) d[u * 32 + lane] = rf[u];
         if (sym)  // mirror chunk stored reversed: both chains then read ascending
 #pragma unroll
             for (int u = 0; u < kPer; ++u)
-                d[kSumChunk / 2 + (kSumChunk / 2 - 1 - (u * 32 + lane))] = make_double2(rb[u].y, rb[u].x);
+                d[kSumChunk / 2 + 1 + (kSumChunk / 2 - 1 - (u * 32 + lane))] = make_double2(rb[u].y, rb[u].x);
     };
-    load(0);
-    stash(0);
-    __syncwarp();
     double acc = 0.0;
     // lanes 0 and 1 run the two chains in lockstep (no divergence): lane 0 ascending over
-    // the block's own chunk, lane 1 descending over the mirror chunk; values are read as
-    // 16-byte pairs ahead of the dependent adds.
+    // the block's own chunk, lane 1 over the reversed mirror chunk. Global loads run two
+    // chunks ahead of the chains; shared reads are software-pipelined ahead of the adds.
     const bool desc = lane == 1;
-    for (int c = 0; c < kChunks; ++c) {
-        if (c + 1 < kChunks) load(c + 1);  // in flight while the chains run
-        const double2* cur = reinterpret_cast<const double2*>(wb + (c & 1) * 2 * kSumChunk +
-                                                               (desc ? kSumChunk : 0));
+    auto chain = [&](int stage) {
+        const double2* cur = reinterpret_cast<const double2*>(wb + stage * kStage) +
+                             (desc ? kSumChunk / 2 + 1 : 0);
         if (lane < 2) {
-            // software pipeline: the adds of group g use registers loaded one group earlier
-            auto fetch = [&](int g, double2 (&v)[8]) {
+            auto fetch = [&](int g, double2 (&v)[4]) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = cur[8 * g + u];
+                for (int u = 0; u < 4; ++u) v[u] = cur[4 * g + u];
             };
-            double2 va[8], vb[8];
+            double2 va[4], vb[4];
             fetch(0, va);
-            constexpr int kGroups = kSumChunk / 16;
+            constexpr int kGroups = kSumChunk / 8;
 #pragma unroll 1
             for (int g = 0; g < kGroups; g += 2) {
                 fetch(g + 1, vb);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     acc = __dadd_rn(acc, va[u].x);
                     acc = __dadd_rn(acc, va[u].y);
                 }
                 if (g + 2 < kGroups) fetch(g + 2, va);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < 4; ++u) {
                     acc = __dadd_rn(acc, vb[u].x);
                     acc = __dadd_rn(acc, vb[u].y);
                 }
             }
         }
+    };
+    load(0, rf0, rb0);
+    load(1, rf1, rb1);
+    stash(0, rf0, rb0);
+    __syncwarp();
+    for (int c = 0; c < kChunks; c += 2) {
+        // even chunk c in stage 0; registers set 1 holds chunk c+1
+        if (c + 2 < kChunks) load(c + 2, rf0, rb0);
+        chain(0);
         __syncwarp();
-        if (c + 1 < kChunks) stash((c + 1) & 1);
+        stash(1, rf1, rb1);
+        __syncwarp();
+        // odd chunk c+1 in stage 1; registers set 0 holds chunk c+2
+        if (c + 3 < kChunks) load(c + 3, rf1, rb1);
+        chain(1);
+        __syncwarp();
+        if (c + 2 < kChunks) stash(0, rf0, rb0);
         __syncwarp();
     }
     double* pp = partials + (size_t)slot * chains;
@@ -667,7 +680,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     if (flags & F_EXPECT) {
         const int nbl = 1 << (Q - 12);
         const int warps = nbl * n_slots;
-        const size_t smem = static_cast<size_t>(kSumWarps) * 2 * 2 * kSumChunk * sizeof(double);
+        const size_t smem = static_cast<size_t>(kSumWarps) * 2 * (2 * kSumChunk + 4) * sizeof(double);
         static bool sum_attr = false;
         if (!sum_attr) {
             QC_CUDA(cudaFuncSetAttribute(k_blocksum, cudaFuncAttributeMaxDynamicSharedMemorySize,
