@@ -301,7 +301,9 @@ def main():
         e2e = {"value": rep_e2e.evals / (sum(t_e2e) / args.steps), "unit": UNIT,
                "h2d_bytes_per_step": (h1 - h0) // args.steps,
                "d2h_bytes_per_step": (d1 - d0) // args.steps,
-               "ms_per_step": sum(t_e2e) / args.steps * 1e3}
+               "ms_per_step": sum(t_e2e) / args.steps * 1e3,
+               "stage_s": {"partition": rep_e2e.partition_s, "qaoa": rep_e2e.qaoa_s,
+                           "merge": rep_e2e.merge_s}}
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

@@ -439,112 +439,88 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 }
 
 // ---------------------------------------------------------------------------
-// blocked expectation over f (statevector.hpp:48-65). One warp per stored 4096-block:
-// the warp streams the block through shared memory (coalesced 16-byte loads, double
-// buffered) while lane 0 runs the ascending chain (the block itself) and, in SYM mode,
-// lane 1 the descending chain (its mirror block in the upper half, 2nbl-1-b). Partials
-// land in full-index block order; the last warp of a slot (atomic ticket) sums them in
-// block order from 0.0 and writes the expectation.
+// blocked expectation over f (statevector.hpp:48-65). Every 4096-block partial is a
+// chain of 4096 dependent adds (8.3-cycle DADD latency on B200 => >= 17 us), so the
+// kernel maximises concurrent chains: each LANE owns one chain. In SYM mode a warp
+// covers 16 stored blocks; lane 2j runs block j ascending (its own partial) and lane
+// 2j+1 runs block j descending (the partial of its mirror block 2nbl-1-j in the upper
+// half). Each lane streams its chain's 64-double chunks into its own shared-memory row
+// with cp.async (3-stage ring, no cross-lane synchronisation) and reads them back in its
+// direction. Partials land in full-index block order; the last warp of a slot (atomic
+// ticket) sums them in block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
-constexpr int kSumWarps = 4;
-constexpr int kSumChunk = 256;  // doubles per chunk (32 KB smem per 4-warp CTA)
+constexpr int kSumChunk = 64;                       // doubles per chunk per chain
+constexpr int kSumRow = kSumChunk + 2;              // row stride (doubles), 16-byte aligned
+constexpr int kSumStages = 3;
+constexpr size_t kSumSmem = static_cast<size_t>(kSumStages) * 32 * kSumRow * sizeof(double);
 
-__global__ void __launch_bounds__(kSumWarps * 32, 4) k_blocksum(const SlotDesc* __restrict__ slots,
-                                                          int n_slots, int Q, int sym,
-                                                          double* __restrict__ partials,
-                                                          unsigned* __restrict__ tickets,
-                                                          double* __restrict__ out) {
-    extern __shared__ double sbuf[];  // [warp][2 stages][fwd, bwd][kSumChunk]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nbl = 1 << (Q - 12);
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ slots, int n_slots,
+                                                int Q, int sym, double* __restrict__ partials,
+                                                unsigned* __restrict__ tickets,
+                                                double* __restrict__ out) {
+    extern __shared__ __align__(16) double srow[];  // [stage][lane][kSumRow]
+    const int lane = threadIdx.x;
+    const int nbl = 1 << (Q - 12);                   // stored blocks per slot
     const int chains = sym ? 2 * nbl : nbl;
-    const int gw = blockIdx.x * kSumWarps + warp;
-    const int slot = gw / nbl;
+    const int bpw = sym ? min(16, nbl) : min(32, nbl);  // blocks per warp
+    const int wps = nbl / bpw;                       // warps per slot
+    const int slot = blockIdx.x / wps;
     if (slot >= n_slots) return;
-    const int b = gw - slot * nbl;
-    const double2* f2 = reinterpret_cast<const double2*>(slots[slot].fbuf + (size_t)b * kBlock);
-    // per warp: 2 stages x {ascending chunk, pad, mirror chunk (reversed), pad}; the pad
-    // keeps the two chain lanes' 16-byte reads in different banks
-    constexpr int kStage = 2 * kSumChunk + 4;
-    double* wb = sbuf + (size_t)warp * 2 * kStage;
-    constexpr int kPer = kSumChunk / 2 / 32;  // double2 per lane per chunk
+    const int b0 = (blockIdx.x - slot * wps) * bpw;
+    const int j = sym ? (lane >> 1) : lane;          // block within the warp
+    const bool desc = sym && (lane & 1);
+    const bool active = j < bpw;
+    const double* fb = slots[slot].fbuf + (size_t)(b0 + (active ? j : 0)) * kBlock;
     constexpr int kChunks = kBlock / kSumChunk;
-    double2 rf0[kPer], rb0[kPer], rf1[kPer], rb1[kPer];
-    auto load = [&](int c, double2 (&rf)[kPer], double2 (&rb)[kPer]) {
+    auto issue = [&](int c) {
+        if (active && c < kChunks) {
+            const double* src = fb + (size_t)(desc ? kChunks - 1 - c : c) * kSumChunk;
+            double* dst = srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow;
 #pragma unroll
-        for (int u = 0; u < kPer; ++u) rf[u] = f2[c * (kSumChunk / 2) + u * 32 + lane];
-        if (sym)
-#pragma unroll
-            for (int u = 0; u < kPer; ++u) rb[u] = f2[(kChunks - 1 - c) * (kSumChunk / 2) + u * 32 + lane];
+            for (int u = 0; u < kSumChunk / 2; ++u) cp_async16_cg(dst + 2 * u, src + 2 * u);
+        }
+        cp_async_commit();
     };
-    auto stash = [&](int stage, const double2 (&rf)[kPer], const double2 (&rb)[kPer]) {
-        double2* d = reinterpret_cast<double2*>(wb + stage * kStage);
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) d[u * 32 + lane] = rf[u];
-        if (sym)  // mirror chunk stored reversed: both chains then read ascending
-#pragma unroll
-            for (int u = 0; u < kPer; ++u)
-                d[kSumChunk / 2 + 1 + (kSumChunk / 2 - 1 - (u * 32 + lane))] = make_double2(rb[u].y, rb[u].x);
-    };
+    issue(0);
+    issue(1);
     double acc = 0.0;
-    // lanes 0 and 1 run the two chains in lockstep (no divergence): lane 0 ascending over
-    // the block's own chunk, lane 1 over the reversed mirror chunk. Global loads run two
-    // chunks ahead of the chains; shared reads are software-pipelined ahead of the adds.
-    const bool desc = lane == 1;
-    auto chain = [&](int stage) {
-        const double2* cur = reinterpret_cast<const double2*>(wb + stage * kStage) +
-                             (desc ? kSumChunk / 2 + 1 : 0);
-        if (lane < 2) {
-            auto fetch = [&](int g, double2 (&v)[4]) {
+    for (int c = 0; c < kChunks; ++c) {
+        issue(c + 2);
+        cp_async_wait<2>();  // this lane's chunk c has landed
+        const double* row = srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow;
+        double v[8];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = cur[4 * g + u];
-            };
-            double2 va[4], vb[4];
-            fetch(0, va);
-            constexpr int kGroups = kSumChunk / 8;
-#pragma unroll 1
-            for (int g = 0; g < kGroups; g += 2) {
-                fetch(g + 1, vb);
+        for (int u = 0; u < 8; ++u) v[u] = row[desc ? kSumChunk - 1 - u : u];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc = __dadd_rn(acc, va[u].x);
-                    acc = __dadd_rn(acc, va[u].y);
-                }
-                if (g + 2 < kGroups) fetch(g + 2, va);
+        for (int k = 0; k < kSumChunk; k += 8) {
+            double nv[8];
+            if (k + 8 < kSumChunk) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc = __dadd_rn(acc, vb[u].x);
-                    acc = __dadd_rn(acc, vb[u].y);
-                }
+                for (int u = 0; u < 8; ++u) nv[u] = row[desc ? kSumChunk - 1 - (k + 8 + u) : (k + 8 + u)];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+            if (k + 8 < kSumChunk) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = nv[u];
             }
         }
-    };
-    load(0, rf0, rb0);
-    load(1, rf1, rb1);
-    stash(0, rf0, rb0);
-    __syncwarp();
-    for (int c = 0; c < kChunks; c += 2) {
-        // even chunk c in stage 0; registers set 1 holds chunk c+1
-        if (c + 2 < kChunks) load(c + 2, rf0, rb0);
-        chain(0);
-        __syncwarp();
-        stash(1, rf1, rb1);
-        __syncwarp();
-        // odd chunk c+1 in stage 1; registers set 0 holds chunk c+2
-        if (c + 3 < kChunks) load(c + 3, rf1, rb1);
-        chain(1);
-        __syncwarp();
-        if (c + 2 < kChunks) stash(0, rf0, rb0);
-        __syncwarp();
     }
     double* pp = partials + (size_t)slot * chains;
-    if (lane == 0) pp[b] = acc;
-    if (lane == 1 && sym) pp[2 * nbl - 1 - b] = acc;
+    if (active) pp[desc ? 2 * nbl - 1 - (b0 + j) : (b0 + j)] = acc;
     __syncwarp();
     if (lane == 0) {
         __threadfence();
         const unsigned ticket = atomicAdd(&tickets[slot], 1u);
-        if (ticket == static_cast<unsigned>(nbl - 1)) {  // last block of this slot
+        if (ticket == static_cast<unsigned>(wps - 1)) {  // last warp of this slot
             __threadfence();
             double total = 0.0;
             for (int k = 0; k < chains; ++k) total = __dadd_rn(total, __ldcg(pp + k));
@@ -679,17 +655,17 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     QC_CUDA(cudaGetLastError());
     if (flags & F_EXPECT) {
         const int nbl = 1 << (Q - 12);
-        const int warps = nbl * n_slots;
-        const size_t smem = static_cast<size_t>(kSumWarps) * 2 * (2 * kSumChunk + 4) * sizeof(double);
+        const int bpw = plan.sym ? std::min(16, nbl) : std::min(32, nbl);
+        const int warps = (nbl / bpw) * n_slots;
         static bool sum_attr = false;
         if (!sum_attr) {
             QC_CUDA(cudaFuncSetAttribute(k_blocksum, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
+                                         static_cast<int>(kSumSmem)));
             sum_attr = true;
         }
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream);
-        k_blocksum<<<(warps + kSumWarps - 1) / kSumWarps, kSumWarps * 32, smem, stream>>>(
-            d_slots, n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+        k_blocksum<<<warps, 32, kSumSmem, stream>>>(d_slots, n_slots, Q, plan.sym ? 1 : 0,
+                                                   d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());
