@@ -449,24 +449,22 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // direction. Partials land in full-index block order; the last warp of a slot (atomic
 // ticket) sums them in block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
-constexpr int kSumChunk = 64;                       // doubles per chunk per chain
+constexpr int kSumChunk = 128;                      // doubles per chunk per chain (1 KB)
 constexpr int kSumRow = kSumChunk + 2;              // row stride (doubles), 16-byte aligned
 constexpr int kSumStages = 3;
-constexpr size_t kSumSmem = static_cast<size_t>(kSumStages) * 32 * kSumRow * sizeof(double);
+constexpr size_t kSumSmem =
+    static_cast<size_t>(kSumStages) * 32 * kSumRow * sizeof(double) + kSumStages * 8;
 
-__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ slots, int n_slots,
                                                 int Q, int sym, double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
-    extern __shared__ __align__(16) double srow[];  // [stage][lane][kSumRow]
+    extern __shared__ __align__(16) double srow[];  // [stage][lane][kSumRow], then mbarriers
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(srow + (size_t)kSumStages * 32 * kSumRow);
     const int lane = threadIdx.x;
     const int nbl = 1 << (Q - 12);                   // stored blocks per slot
     const int chains = sym ? 2 * nbl : nbl;
@@ -478,23 +476,54 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
     const int j = sym ? (lane >> 1) : lane;          // block within the warp
     const bool desc = sym && (lane & 1);
     const bool active = j < bpw;
+    const int n_active = sym ? 2 * bpw : bpw;
     const double* fb = slots[slot].fbuf + (size_t)(b0 + (active ? j : 0)) * kBlock;
     constexpr int kChunks = kBlock / kSumChunk;
+    constexpr unsigned kBytes = kSumChunk * sizeof(double);
+    if (lane < kSumStages) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + lane)) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncwarp();
+    // TMA bulk copy of this lane's next chunk into its own row; lane 0 arms the stage's
+    // barrier with the bytes all active lanes will deliver
     auto issue = [&](int c) {
-        if (active && c < kChunks) {
-            const double* src = fb + (size_t)(desc ? kChunks - 1 - c : c) * kSumChunk;
-            double* dst = srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow;
-#pragma unroll
-            for (int u = 0; u < kSumChunk / 2; ++u) cp_async16_cg(dst + 2 * u, src + 2 * u);
+        if (c >= kChunks) return;
+        const int st = c % kSumStages;
+        if (lane == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(
+                             smem_u32(mbar + st)),
+                         "r"(kBytes * static_cast<unsigned>(n_active))
+                         : "memory");
         }
-        cp_async_commit();
+        if (active) {
+            const double* src = fb + (size_t)(desc ? kChunks - 1 - c : c) * kSumChunk;
+            double* dst = srow + ((size_t)st * 32 + lane) * kSumRow;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_u32(dst)),
+                "l"(src), "r"(kBytes), "r"(smem_u32(mbar + st))
+                : "memory");
+        }
+    };
+    auto wait = [&](int c) {
+        const unsigned addr = smem_u32(mbar + c % kSumStages);
+        const unsigned parity = static_cast<unsigned>((c / kSumStages) & 1);
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(addr), "r"(parity)
+                : "memory");
+        }
     };
     issue(0);
     issue(1);
     double acc = 0.0;
     for (int c = 0; c < kChunks; ++c) {
         issue(c + 2);
-        cp_async_wait<2>();  // this lane's chunk c has landed
+        wait(c);
         const double* row = srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow;
         double v[8];
 #pragma unroll
@@ -513,6 +542,7 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
                 for (int u = 0; u < 8; ++u) v[u] = nv[u];
             }
         }
+        __syncwarp();  // every lane is done with this stage before it is refilled
     }
     double* pp = partials + (size_t)slot * chains;
     if (active) pp[desc ? 2 * nbl - 1 - (b0 + j) : (b0 + j)] = acc;
