@@ -441,12 +441,11 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // ---------------------------------------------------------------------------
 // blocked expectation over f (statevector.hpp:48-65). Every 4096-block partial is a
 // chain of 4096 dependent adds (8.3-cycle DADD latency on B200 => >= 17 us), so the
-// kernel maximises concurrent chains: each LANE owns one chain. In SYM mode a warp
-// covers 16 stored blocks; lane 2j runs block j ascending (its own partial) and lane
-// 2j+1 runs block j descending (the partial of its mirror block 2nbl-1-j in the upper
-// half). Each lane streams its chain's 64-double chunks into its own shared-memory row
-// with cp.async (3-stage ring, no cross-lane synchronisation) and reads them back in its
-// direction. Partials land in full-index block order; the last warp of a slot (atomic
+// kernel maximises concurrent chains: each LANE owns one chain. A warp covers up to 32
+// stored blocks in one direction: ascending warps produce the blocks' own partials,
+// descending warps (SYM) those of the mirror blocks 2nbl-1-b in the upper half. Each
+// lane's next 1 KB chunk arrives by a TMA bulk copy (cp.async.bulk, mbarrier ring of 3
+// stages) into its own shared-memory row. Partials land in full-index block order; the last warp of a slot (atomic
 // ticket) sums them in block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
 constexpr int kSumChunk = 128;                      // doubles per chunk per chain (1 KB)
@@ -468,15 +467,19 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
     const int lane = threadIdx.x;
     const int nbl = 1 << (Q - 12);                   // stored blocks per slot
     const int chains = sym ? 2 * nbl : nbl;
-    const int bpw = sym ? min(16, nbl) : min(32, nbl);  // blocks per warp
-    const int wps = nbl / bpw;                       // warps per slot
+    // direction-uniform warps: each covers up to 32 stored blocks in ONE direction (SYM:
+    // ascending warps then descending warps), so every lane of a warp runs the same code
+    const int bpw = min(32, nbl);                    // blocks per warp
+    const int wpd = nbl / bpw;                       // warps per direction per slot
+    const int wps = sym ? 2 * wpd : wpd;             // warps per slot
     const int slot = blockIdx.x / wps;
     if (slot >= n_slots) return;
-    const int b0 = (blockIdx.x - slot * wps) * bpw;
-    const int j = sym ? (lane >> 1) : lane;          // block within the warp
-    const bool desc = sym && (lane & 1);
+    const int wis = blockIdx.x - slot * wps;
+    const bool desc = wis >= wpd;
+    const int b0 = (desc ? wis - wpd : wis) * bpw;
+    const int j = lane;
     const bool active = j < bpw;
-    const int n_active = sym ? 2 * bpw : bpw;
+    const int n_active = bpw;
     const double* fb = slots[slot].fbuf + (size_t)(b0 + (active ? j : 0)) * kBlock;
     constexpr int kChunks = kBlock / kSumChunk;
     constexpr unsigned kBytes = kSumChunk * sizeof(double);
@@ -521,28 +524,54 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
     issue(0);
     issue(1);
     double acc = 0.0;
-    for (int c = 0; c < kChunks; ++c) {
-        issue(c + 2);
-        wait(c);
-        const double* row = srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow;
-        double v[8];
+    // 16-byte reads (row stride 130 doubles: 8 lanes fill one 128-byte wavefront)
+    constexpr int kPairs = kSumChunk / 2;
+    if (!desc) {
+        for (int c = 0; c < kChunks; ++c) {
+            issue(c + 2);
+            wait(c);
+            const double2* r = reinterpret_cast<const double2*>(srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow);
+            double2 v[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = row[desc ? kSumChunk - 1 - u : u];
+            for (int u = 0; u < 4; ++u) v[u] = r[u];
 #pragma unroll
-        for (int k = 0; k < kSumChunk; k += 8) {
-            double nv[8];
-            if (k + 8 < kSumChunk) {
+            for (int k = 0; k < kPairs; k += 4) {
+                double2 nv[4];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) nv[u] = row[desc ? kSumChunk - 1 - (k + 8 + u) : (k + 8 + u)];
+                for (int u = 0; u < 4; ++u) nv[u] = r[(k + 4 + u) & (kPairs - 1)];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __dadd_rn(acc, v[u].x);
+                    acc = __dadd_rn(acc, v[u].y);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = nv[u];
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
-            if (k + 8 < kSumChunk) {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = nv[u];
-            }
+            __syncwarp();  // every lane is done with this stage before it is refilled
         }
-        __syncwarp();  // every lane is done with this stage before it is refilled
+    } else {
+        for (int c = 0; c < kChunks; ++c) {
+            issue(c + 2);
+            wait(c);
+            const double2* r = reinterpret_cast<const double2*>(srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow);
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = r[kPairs - 1 - u];
+#pragma unroll
+            for (int k = 0; k < kPairs; k += 4) {
+                double2 nv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) nv[u] = r[(kPairs - 1 - (k + 4 + u)) & (kPairs - 1)];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc = __dadd_rn(acc, v[u].y);
+                    acc = __dadd_rn(acc, v[u].x);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = nv[u];
+            }
+            __syncwarp();
+        }
     }
     double* pp = partials + (size_t)slot * chains;
     if (active) pp[desc ? 2 * nbl - 1 - (b0 + j) : (b0 + j)] = acc;
@@ -685,8 +714,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     QC_CUDA(cudaGetLastError());
     if (flags & F_EXPECT) {
         const int nbl = 1 << (Q - 12);
-        const int bpw = plan.sym ? std::min(16, nbl) : std::min(32, nbl);
-        const int warps = (nbl / bpw) * n_slots;
+        const int bpw = std::min(32, nbl);
+        const int warps = (nbl / bpw) * (plan.sym ? 2 : 1) * n_slots;
         static bool sum_attr = false;
         if (!sum_attr) {
             QC_CUDA(cudaFuncSetAttribute(k_blocksum, cudaFuncAttributeMaxDynamicSharedMemorySize,
