@@ -163,10 +163,11 @@ struct ChainStats {
 int launch_levels(const uint32_t* d_eu, const uint32_t* d_ev, const double* d_ew, int m,
                   int Q, bool integral, uint16_t* d_lev, double* d_val, cudaStream_t stream);
 // d_tickets: n_slots zero-initialised counters (left zeroed on return).
+// d_fbuf: the f buffer of slot 0 of this launch (slots contiguous, 2^Q doubles each).
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
-                 int n_slots, int p, uint32_t flags, double* d_partials, unsigned* d_tickets,
-                 double* d_out, cudaStream_t stream, const ChainStats* stats = nullptr,
-                 Prof* prof = nullptr);
+                 int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
+                 unsigned* d_tickets, double* d_out, cudaStream_t stream,
+                 const ChainStats* stats = nullptr, Prof* prof = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
 
 // Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,

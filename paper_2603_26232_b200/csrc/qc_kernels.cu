@@ -22,9 +22,11 @@
 //                          mirror op last; the final one emits f(z)=|a|^2 C(z)
 //   k_blocksum: the blocked sequential expectation over f (+ the in-order block sum).
 // Q <= 12 (k_onchip): the whole state lives in one CTA's shared memory for all layers.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <cstdint>
 
 #include "qc_internal.hpp"
@@ -448,22 +450,29 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // stages) into its own shared-memory row. Partials land in full-index block order; the last warp of a slot (atomic
 // ticket) sums them in block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
-constexpr int kSumChunk = 128;                      // doubles per chunk per chain (1 KB)
-constexpr int kSumRow = kSumChunk + 2;              // row stride (doubles), 16-byte aligned
+constexpr int kSumParts = 8;                        // 16-double parts per chunk
+constexpr int kSumChunk = 16 * kSumParts;           // doubles per chunk per chain (1 KB)
 constexpr int kSumStages = 3;
-constexpr size_t kSumSmem =
-    static_cast<size_t>(kSumStages) * 32 * kSumRow * sizeof(double) + kSumStages * 8;
+constexpr size_t kSumStageBytes = 32 * kSumChunk * sizeof(double);  // 32 KB
+constexpr size_t kSumSmem = kSumStages * kSumStageBytes + 1024 + kSumStages * 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-__global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ slots, int n_slots,
-                                                int Q, int sym, double* __restrict__ partials,
+// tmap: the f buffer of the launch as a 3-D tensor {16 doubles, block (32 KB stride),
+// part (128 B stride)}, box {16, 32, kSumParts}, 128-byte swizzle: the shared box is
+// [part][block][16 doubles] and 16-byte unit u of row r sits at unit u ^ (r & 7), so the
+// 32 lanes (one block each) read one part conflict-free.
+__global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
+                                                int n_slots, int Q, int sym,
+                                                double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
-    extern __shared__ __align__(16) double srow[];  // [stage][lane][kSumRow], then mbarriers
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(srow + (size_t)kSumStages * 32 * kSumRow);
+    extern __shared__ unsigned char sraw[];
+    unsigned char* sbase = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(sraw) + 1023) & ~uintptr_t{1023});
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + kSumStages * kSumStageBytes);
     const int lane = threadIdx.x;
     const int nbl = 1 << (Q - 12);                   // stored blocks per slot
     const int chains = sym ? 2 * nbl : nbl;
@@ -476,38 +485,26 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
     if (slot >= n_slots) return;
     const int wis = blockIdx.x - slot * wps;
     const bool desc = wis >= wpd;
-    const int b0 = (desc ? wis - wpd : wis) * bpw;
-    const int j = lane;
-    const bool active = j < bpw;
-    const int n_active = bpw;
-    const double* fb = slots[slot].fbuf + (size_t)(b0 + (active ? j : 0)) * kBlock;
+    const int b0 = (desc ? wis - wpd : wis) * bpw;   // first block (within the slot)
+    const int gb0 = slot * nbl + b0;                 // first block (tensor coordinate)
     constexpr int kChunks = kBlock / kSumChunk;
-    constexpr unsigned kBytes = kSumChunk * sizeof(double);
-    if (lane < kSumStages) {
+    if (lane < kSumStages)
         asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + lane)) : "memory");
-    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncwarp();
-    // TMA bulk copy of this lane's next chunk into its own row; lane 0 arms the stage's
-    // barrier with the bytes all active lanes will deliver
     auto issue = [&](int c) {
-        if (c >= kChunks) return;
+        if (c >= kChunks || lane != 0) return;
         const int st = c % kSumStages;
-        if (lane == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(
-                             smem_u32(mbar + st)),
-                         "r"(kBytes * static_cast<unsigned>(n_active))
-                         : "memory");
-        }
-        if (active) {
-            const double* src = fb + (size_t)(desc ? kChunks - 1 - c : c) * kSumChunk;
-            double* dst = srow + ((size_t)st * 32 + lane) * kSumRow;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                    smem_u32(dst)),
-                "l"(src), "r"(kBytes), "r"(smem_u32(mbar + st))
-                : "memory");
-        }
+        const int part0 = (desc ? kChunks - 1 - c : c) * kSumParts;
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar + st)),
+                     "r"(static_cast<unsigned>(kSumStageBytes))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(sbase + st * kSumStageBytes)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(gb0), "r"(part0),
+            "r"(smem_u32(mbar + st))
+            : "memory");
     };
     auto wait = [&](int c) {
         const unsigned addr = smem_u32(mbar + c % kSumStages);
@@ -524,57 +521,42 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
     issue(0);
     issue(1);
     double acc = 0.0;
-    // 16-byte reads (row stride 130 doubles: 8 lanes fill one 128-byte wavefront)
-    constexpr int kPairs = kSumChunk / 2;
-    if (!desc) {
-        for (int c = 0; c < kChunks; ++c) {
-            issue(c + 2);
-            wait(c);
-            const double2* r = reinterpret_cast<const double2*>(srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow);
-            double2 v[4];
+    const unsigned sw = static_cast<unsigned>(lane & 7);
+    for (int c = 0; c < kChunks; ++c) {
+        issue(c + 2);
+        wait(c);
+        const unsigned char* st = sbase + (c % kSumStages) * kSumStageBytes;
+        if (!desc) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = r[u];
+            for (int p = 0; p < kSumParts; ++p) {
+                const double2* row = reinterpret_cast<const double2*>(st + (p * 32 + lane) * 128);
+                double2 v[8];
 #pragma unroll
-            for (int k = 0; k < kPairs; k += 4) {
-                double2 nv[4];
+                for (int u = 0; u < 8; ++u) v[u] = row[u ^ sw];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) nv[u] = r[(k + 4 + u) & (kPairs - 1)];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 8; ++u) {
                     acc = __dadd_rn(acc, v[u].x);
                     acc = __dadd_rn(acc, v[u].y);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = nv[u];
             }
-            __syncwarp();  // every lane is done with this stage before it is refilled
-        }
-    } else {
-        for (int c = 0; c < kChunks; ++c) {
-            issue(c + 2);
-            wait(c);
-            const double2* r = reinterpret_cast<const double2*>(srow + ((size_t)(c % kSumStages) * 32 + lane) * kSumRow);
-            double2 v[4];
+        } else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = r[kPairs - 1 - u];
+            for (int p = kSumParts - 1; p >= 0; --p) {
+                const double2* row = reinterpret_cast<const double2*>(st + (p * 32 + lane) * 128);
+                double2 v[8];
 #pragma unroll
-            for (int k = 0; k < kPairs; k += 4) {
-                double2 nv[4];
+                for (int u = 0; u < 8; ++u) v[u] = row[(7 - u) ^ sw];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) nv[u] = r[(kPairs - 1 - (k + 4 + u)) & (kPairs - 1)];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 8; ++u) {
                     acc = __dadd_rn(acc, v[u].y);
                     acc = __dadd_rn(acc, v[u].x);
                 }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = nv[u];
             }
-            __syncwarp();
         }
+        __syncwarp();  // every lane is done with this stage before it is refilled
     }
     double* pp = partials + (size_t)slot * chains;
-    if (active) pp[desc ? 2 * nbl - 1 - (b0 + j) : (b0 + j)] = acc;
+    if (lane < bpw) pp[desc ? 2 * nbl - 1 - (b0 + lane) : (b0 + lane)] = acc;
     __syncwarp();
     if (lane == 0) {
         __threadfence();
@@ -587,6 +569,34 @@ __global__ void __launch_bounds__(32) k_blocksum(const SlotDesc* __restrict__ sl
             tickets[slot] = 0u;
         }
     }
+}
+
+// Encode the f-buffer tensor map (driver entry point resolved once through the runtime).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static CUtensorMap fbuf_tensor_map(double* fbuf, uint64_t total_blocks) {
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        QC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) internal_error("cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {16, total_blocks, kBlock / 16};
+    const cuuint64_t strides[2] = {kBlock * sizeof(double), 16 * sizeof(double)};
+    const cuuint32_t box[3] = {16, 32, kSumParts};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, fbuf, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) internal_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -647,8 +657,9 @@ size_t partials_per_slot(const ChainPlan& plan) {
 }
 
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
-                 int n_slots, int p, uint32_t flags, double* d_partials, unsigned* d_tickets,
-                 double* d_out, cudaStream_t stream, const ChainStats* stats, Prof* prof) {
+                 int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
+                 unsigned* d_tickets, double* d_out, cudaStream_t stream, const ChainStats* stats,
+                 Prof* prof) {
     if (n_slots <= 0) return 0;
     const int Q = plan.Q;
     const double N = static_cast<double>(size_t{1} << Q);
@@ -722,9 +733,10 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                                          static_cast<int>(kSumSmem)));
             sum_attr = true;
         }
+        const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream);
-        k_blocksum<<<warps, 32, kSumSmem, stream>>>(d_slots, n_slots, Q, plan.sym ? 1 : 0,
-                                                   d_partials, d_tickets, d_out);
+        k_blocksum<<<warps, 32, kSumSmem, stream>>>(tmap, n_slots, Q, plan.sym ? 1 : 0, d_partials,
+                                                   d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());
