@@ -326,6 +326,13 @@ class OracleLib(_Lib):
     def __init__(self):
         super().__init__(ORACLE_SO)
 
+    def set_qubit_cap(self, cap: int):
+        """kQubitCap (statevector.hpp:20): 24 in the reference, 26 for config 5."""
+        self.lib.orc_set_qubit_cap(C.c_int(cap))
+
+    def qubit_cap(self) -> int:
+        return self.lib.orc_qubit_cap()
+
 
 def ref_available(cap26: bool = False) -> bool:
     return os.path.exists(REF26_SO if cap26 else REF_SO)

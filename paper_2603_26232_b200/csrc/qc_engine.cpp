@@ -380,7 +380,10 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             const size_t per = e->chunk_slots(plan.Q, plan.onchip, ns);
             const size_t nchunks = (ns + per - 1) / per;
             e->reserve(plan.Q, !plan.onchip, ns);
-            std::vector<ChunkCtx> ctx(nchunks);
+            while (e->chunk_pool.size() < nchunks) e->chunk_pool.push_back(std::make_unique<ChunkCtx>());
+            std::vector<ChunkCtx*> ctxp(nchunks);
+            for (size_t c = 0; c < nchunks; ++c) ctxp[c] = e->chunk_pool[c].get();
+            auto ctx = [&](size_t c) -> ChunkCtx& { return *ctxp[c]; };
             // the aux stream must see the cut tables / zeroed tickets written on the main one
             cudaEvent_t ready;
             QC_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -391,7 +394,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             for (size_t k = 0; k + 1 < nstreams; ++k) QC_CUDA(cudaStreamWaitEvent(e->aux[k], ready, 0));
             QC_CUDA(cudaEventDestroy(ready));
             for (size_t c = 0; c < nchunks; ++c)
-                ctx[c].st = (c % nstreams) ? e->aux[c % nstreams - 1] : e->stream;
+                ctx(c).st = (c % nstreams) ? e->aux[c % nstreams - 1] : e->stream;
             std::vector<std::vector<EvalPoint>> pts(nchunks);
             std::vector<std::vector<size_t>> who(nchunks);
             std::vector<char> inflight(nchunks, 0);
@@ -409,7 +412,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                 inflight[c] = !pts[c].empty();
                 if (inflight[c])
                     e->enqueue_chunk(dg, pts[c].data(), static_cast<int>(pts[c].size()), p,
-                                     F_INIT | F_EXPECT, c * per, ctx[c]);
+                                     F_INIT | F_EXPECT, c * per, ctx(c));
             };
             for (size_t c = 0; c < nchunks; ++c) launch(c);
             bool any = true;
@@ -418,7 +421,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                 for (size_t c = 0; c < nchunks; ++c) {
                     if (!inflight[c]) continue;
                     vals.assign(pts[c].size(), 0.0);
-                    e->wait_chunk(ctx[c], vals.data());
+                    e->wait_chunk(ctx(c), vals.data());
                     for (size_t k = 0; k < who[c].size(); ++k) {
                         const size_t i = who[c][k];
                         const double f = -vals[k];  // qaoa.hpp:90

@@ -9,6 +9,8 @@
 
 #include "../../include/qcgpu.h"
 #include "qc_internal.hpp"
+#include "qc_merge.hpp"
+#include <memory>
 
 namespace qcg {
 
@@ -81,6 +83,8 @@ struct qc_engine {
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
     qcg::HostBuf hstage, hout;
     qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
+    qcg::DeviceArena merge_arena;                           // merge scratch, reused
+    std::vector<std::unique_ptr<qcg::ChunkCtx>> chunk_pool;  // per-chunk staging, reused
     uint64_t h2d = 0, d2h = 0;  // bytes copied host<->device by this engine
 
     // Build the device cut tables of graphs (sym: half state) into `target` (default:

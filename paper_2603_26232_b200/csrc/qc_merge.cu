@@ -405,10 +405,17 @@ __global__ void k_cut_int(const uint32_t* __restrict__ eu, const uint32_t* __res
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+thread_local DeviceArena* g_arena = nullptr;
+
 template <typename T>
 T* dalloc(std::vector<void*>& keep, size_t n) {
-    void* p = nullptr;
     if (n == 0) n = 1;
+    if (g_arena) {
+        void* p = g_arena->get(n * sizeof(T));
+        if (!p) resource_error("device out of memory (merge scratch)");
+        return static_cast<T*>(p);
+    }
+    void* p = nullptr;
     QC_CUDA(cudaMalloc(&p, n * sizeof(T)));
     keep.push_back(p);
     return static_cast<T*>(p);
@@ -463,7 +470,8 @@ double estimate_paths(const int32_t* counts, int M, bool halve) {
 }
 
 MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
-                      cudaStream_t st, uint64_t* launches, Prof* prof, uint64_t* h2d, uint64_t* d2h) {
+                      cudaStream_t st, uint64_t* launches, Prof* prof, uint64_t* h2d, uint64_t* d2h,
+                      DeviceArena* arena) {
     Prof dummy;
     if (!prof) prof = &dummy;
     uint64_t h2d_local = 0, d2h_local = 0;
@@ -477,9 +485,12 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         ~Freer() {
             for (void* p : *k) cudaFree(p);
             g_h2d_counter = nullptr;
+            g_arena = nullptr;
         }
     } freer{&keep};
     g_h2d_counter = h2d;
+    g_arena = arena;
+    if (arena) arena->reset();
     auto S = [](int i) { return static_cast<size_t>(i); };
 
     // ---- first level of every vertex (merge.hpp:106-108), integrality

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
+#include <utility>
 #include <vector>
 
 namespace qcg {
@@ -42,9 +44,38 @@ void check_pool(const MergeInput& in);
 double estimate_paths(const int32_t* counts, int M, bool halve);
 // Runs the windows back to back on `st` and returns the re-scored result.
 // full_graph selects MergeEval::kFullGraph scoring (merge.hpp:164) on the exact path.
+// Device scratch reused across merges (allocation i of a call reuses buffer i).
+struct DeviceArena {
+    std::deque<std::pair<void*, size_t>> bufs;
+    size_t next = 0;
+    void reset() { next = 0; }
+    void* get(size_t bytes) {
+        if (bytes == 0) bytes = 16;
+        if (next == bufs.size()) bufs.emplace_back(nullptr, 0);
+        auto& b = bufs[next++];
+        if (b.second < bytes) {
+            if (b.first) cudaFree(b.first);
+            b.first = nullptr;
+            b.second = 0;
+            if (cudaMalloc(&b.first, bytes) != cudaSuccess) {
+                (void)cudaGetLastError();
+                b.first = nullptr;
+                return nullptr;
+            }
+            b.second = bytes;
+        }
+        return b.first;
+    }
+    ~DeviceArena() {
+        for (auto& b : bufs)
+            if (b.first) cudaFree(b.first);
+    }
+};
+
 struct Prof;
 MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
                       cudaStream_t st, uint64_t* launches, Prof* prof = nullptr,
-                      uint64_t* h2d = nullptr, uint64_t* d2h = nullptr);
+                      uint64_t* h2d = nullptr, uint64_t* d2h = nullptr,
+                      DeviceArena* arena = nullptr);
 
 }  // namespace qcg

@@ -195,7 +195,7 @@ MergeOutput level_merge(qc_engine* e, const MergeInput& in, int start_level, int
         resource_error("start level " + std::to_string(start_level) + " expands to about " +
                        std::to_string(prefix_est) + " prefixes; lower it");
     return run_merge(in, {Window{0, M, halve ? 3 : 2}}, !incremental, e->stream, &e->launches,
-                     &e->prof, &e->h2d, &e->d2h);
+                     &e->prof, &e->h2d, &e->d2h, &e->merge_arena);
 }
 
 // merge.hpp:345-412 chained_merge
@@ -229,7 +229,8 @@ MergeOutput chained_merge(qc_engine* e, const MergeInput& in, long long window,
         wins.push_back({s, e_, s == 0 ? (halve ? 3 : 2) : -1});
         s = e_;
     }
-    return run_merge(in, wins, false, e->stream, &e->launches, &e->prof, &e->h2d, &e->d2h);
+    return run_merge(in, wins, false, e->stream, &e->launches, &e->prof, &e->h2d, &e->d2h,
+                     &e->merge_arena);
 }
 
 Pool pool_from_c(const qc_pool* p) {
