@@ -376,6 +376,7 @@ def main():
                    "l2": "working set (21 half-states x 8 MiB + f buffers) > 126 MB L2; "
                          "L2 flushed (256 MB write) between timed steps"},
         "solve_time_s": sec_per_step, "cut": rep.cut, "evals_per_step": evals_per_step,
+        "step_ms": [round(t * 1e3, 2) for t in t_val],
         "stage_s": {"partition": rep.partition_s, "qaoa": rep.qaoa_s, "merge": rep.merge_s},
         "e2e": e2e, "gpu_launches": int(lt.item()), "clocks": clk, "roofline": roofline,
     }
