@@ -3,6 +3,8 @@
 The lockstep ask/tell Nelder-Mead must reproduce every (x, f) of the reference
 trajectory; SolveResults, merge results and the config-1 cut must be identical.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -200,3 +202,45 @@ def test_config1_pipeline(engine, oracle):
                               "101110001111110110000000101100001011")
     assert rep.candidates_evaluated == 8388608
     assert rep.subgraphs == 11 and not rep.windowed
+
+
+# ---- multi-GPU record path, emulated in one process -------------------------------------
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_sharded_records_equal_single_gpu(engine, oracle, shards):
+    from paper_2603_26232_b200 import kcap_for
+    e = oracle.generate_er(100, 0.1, 0)
+    cfg = dict(qubit_cap=10, top_k=4, layers=1, budget=200, seed=0)
+    M = engine.subgraph_count(100, e, **cfg)
+    rb = engine.record_bytes(kcap_for(10, 4), 1)
+    recs = []
+    for r in range(shards):
+        b, en = engine.shard_range(M, r, shards)
+        recs.append(engine.shard_solve(100, e, b, en, rb, **cfg))
+    rep = engine.merge_records(100, e, np.concatenate(recs), M, **cfg)
+    single = engine.run_pipeline(100, e, **cfg)
+    assert rep.cut == single.cut == 296.0
+    assert rep.assignment == single.assignment
+    assert rep.candidates_evaluated == single.candidates_evaluated
+    assert rep.evals == single.evals == 11 * 200
+
+
+def test_pipeline_windowed_matches_oracle(engine, oracle):
+    e = oracle.generate_er(120, 0.2, 5)
+    kw = dict(qubit_cap=8, top_k=3, layers=1, budget=30, seed=2, path_budget=1e5)
+    ref = oracle.run_pipeline(120, e, **kw)
+    got = engine.run_pipeline(120, e, **kw)
+    assert ref["windowed"] and got.windowed
+    assert got.cut == ref["cut"] and got.assignment == ref["assignment"]
+    assert got.candidates_evaluated == ref["leaves"]
+
+
+def test_pipeline_c2_shape_matches_oracle(engine, oracle):
+    """config-2 shape (400 vertices, 20-qubit pieces) with a short NM budget so the
+    oracle finishes quickly; the full budget runs in bench.py."""
+    e = oracle.generate_er(400, 0.1, 0)
+    kw = dict(qubit_cap=20, top_k=2, layers=2, budget=8, seed=0)
+    ref = oracle.run_pipeline(400, e, workers=os.cpu_count() or 1, **kw)
+    got = engine.run_pipeline(400, e, **kw)
+    assert got.cut == ref["cut"] and got.assignment == ref["assignment"]
+    assert got.candidates_evaluated == ref["leaves"]
+    assert np.array_equal(np.array([got.evals]), np.array([int(ref["sub_evals"].sum())]))
