@@ -75,7 +75,7 @@ def er_graph(n, p, seed):
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled every 200 ms during the timed region, in-process
+    """SM/memory clocks, power, temperature and throttle reasons sampled every 100 ms during the timed region, in-process
     through NVML (the same counters nvidia-smi reports; a polling nvidia-smi process was
     observed to stall the driver and inflate individual steps by 35-65 ms)."""
 
@@ -87,6 +87,7 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.samples = []
+        self.mem, self.power, self.temp = [], [], []
         self.reasons = set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -103,13 +104,16 @@ class ClockSampler:
                 while not self._stop.is_set():
                     try:
                         self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        self.mem.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM)))
+                        self.power.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                        self.temp.append(float(pynvml.nvmlDeviceGetTemperature(h, pynvml.NVML_TEMPERATURE_GPU)))
                         bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                         for nm, b in self.REASONS.items():
                             if bits & b:
                                 self.reasons.add(nm)
                     except Exception:
                         pass
-                    self._stop.wait(0.2)
+                    self._stop.wait(0.1)
             self.thread = threading.Thread(target=loop, daemon=True)
             self.thread.start()
         except Exception:
@@ -121,8 +125,12 @@ class ClockSampler:
         self._stop.set()
         self.thread.join(timeout=2)
         return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_min_mhz": min(self.samples) if self.samples else None,
                 "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
-                "reasons": sorted(self.reasons), "source": "NVML (in-process)"}
+                "mem_mhz": [min(self.mem), max(self.mem)] if self.mem else None,
+                "power_w_max": max(self.power) if self.power else None,
+                "temp_c_max": max(self.temp) if self.temp else None,
+                "reasons": sorted(self.reasons), "source": "NVML (in-process, 100 ms)"}
 
 
 # --------------------------------------------------------------------------------------
@@ -199,6 +207,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-stride", type=int, default=PROFILE_STRIDE,
+                    help="CUDA-event sampling of 1 launch in N during the timed region (0: off)")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload])
     if args.impl == "reference":
@@ -246,8 +256,8 @@ def main():
         """per-step device time via CUDA events on the engine stream, L2 flushed between."""
         times, last = [], None
         launches0 = eng.launches
-        if prof:
-            eng.profile(PROFILE_STRIDE)
+        if prof and args.profile_stride > 0:
+            eng.profile(args.profile_stride)
         for _ in range(steps):
             flush.zero_()
             barrier()
@@ -259,7 +269,7 @@ def main():
             barrier()
             times.append(ev0.elapsed_time(ev1) / 1e3)
         launches = eng.launches - launches0
-        profile = eng.profile_read() if prof else None
+        profile = eng.profile_read() if prof and args.profile_stride > 0 else {}
         if prof:
             eng.profile(False)
         return times, last, launches, profile
@@ -356,7 +366,7 @@ def main():
                 "step_aggregate_GBs": iso_bytes / sec_per_step / 1e9,
                 "step_aggregate_frac": iso_bytes / sec_per_step / 1e9 / peak,
                 "timed_region_sampled": {
-                    "stride": PROFILE_STRIDE, "streams": 3,
+                    "stride": args.profile_stride, "streams": 3,
                     "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                     "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
                                     if v["ms"] > 0 else 0.0}

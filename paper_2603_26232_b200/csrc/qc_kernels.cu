@@ -446,209 +446,6 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 }
 
 // ---------------------------------------------------------------------------
-// Persistent variants (QCG_PERSIST=1): one 512-thread CTA per SM walks its tiles with a
-// two-stage cp.async ring, so tile k+1's amplitudes (and levels) stream in while tile k
-// runs its rounds. Same rounds/layouts as above.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32_any(smem)), "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-
-constexpr size_t kPersistLowSmem = 2 * 4096 * sizeof(double2) + 2 * 4096 * sizeof(uint16_t) +
-                                   kLutSmem * sizeof(double2);
-
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass_low_p(const SlotDesc* __restrict__ slots,
-                                                              const LayerParam* __restrict__ lp,
-                                                              int layer, int Q, uint32_t flags,
-                                                              uint32_t total_tiles) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    double2* buf = reinterpret_cast<double2*>(smraw);                                  // [2][4096]
-    uint16_t* levs = reinterpret_cast<uint16_t*>(smraw + 2 * 4096 * sizeof(double2));  // [2][4096]
-    double2* slut = reinterpret_cast<double2*>(smraw + 2 * 4096 * sizeof(double2) + 2 * 4096 * 2);
-    const int tshift = Q - 12;
-    const uint32_t tmask = (1u << tshift) - 1u;
-    const bool init = flags & F_INIT;
-    const uint32_t tid = threadIdx.x;
-    auto issue = [&](uint32_t t, int stage) {
-        if (t < total_tiles) {
-            const SlotDesc& S = slots[t >> tshift];
-            const LayerParam& L = lp[S.layer_base + layer];
-            if (init || L.phase || L.mix) {
-                const uint32_t base = (t & tmask) << 12;
-                if (!init) {
-                    const double2* src = S.state + base;
-                    double2* dst = buf + stage * 4096;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        cpa16(dst + swz(k * kPassThreads + tid), src + k * kPassThreads + tid);
-                }
-                if (L.phase && S.lev) cpa16(levs + stage * 4096 + tid * 8, S.lev + base + tid * 8);
-            }
-        }
-        cpa_commit();
-    };
-    uint32_t t = blockIdx.x;
-    issue(t, 0);
-    for (int k = 0; t < total_tiles; ++k, t += gridDim.x) {
-        const int stage = k & 1;
-        issue(t + gridDim.x, stage ^ 1);
-        const SlotDesc S = slots[t >> tshift];
-        const LayerParam L = lp[S.layer_base + layer];
-        const bool use_lev = L.phase && S.lev;
-        const bool lut_sm = use_lev && L.lut_len <= kLutSmem;
-        if (lut_sm)
-            for (int i = tid; i < L.lut_len; i += kPassThreads) slut[i] = L.lut[i];
-        cpa_wait1();
-        __syncthreads();
-        if (init || L.phase || L.mix) {
-            const uint32_t base = (t & tmask) << 12;
-            double2* sm = buf + stage * 4096;
-            const uint4 lv4 = use_lev ? *reinterpret_cast<const uint4*>(levs + stage * 4096 + tid * 8)
-                                      : make_uint4(0, 0, 0, 0);
-            const uint32_t lvw[4] = {lv4.x, lv4.y, lv4.z, lv4.w};
-            double2 a[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t e = tid * 8u + j;
-                double2 v = init ? make_double2(S.amp0, 0.0) : sm[swz(e)];
-                if (L.phase) {
-                    if (use_lev) {
-                        const uint32_t lev = (lvw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-                        v = cmul_rn(v, lut_sm ? slut[lev] : L.lut[lev]);
-                    } else {
-                        v = phase_rn(v, S, L, base + e);
-                    }
-                }
-                a[j] = v;
-            }
-            if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sm[swz(tid * 8u + j)] = a[j];
-            __syncthreads();
-            {
-                const uint32_t r = ((tid >> 3) << 6) | (tid & 7u);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 3))];
-                if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) sm[swz(r | (j << 3))] = a[j];
-            }
-            __syncthreads();
-            {
-                const uint32_t r = ((tid >> 6) << 9) | (tid & 63u);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 6))];
-                if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) sm[swz(r | (j << 6))] = a[j];
-            }
-            __syncthreads();
-#pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = sm[swz((j << 9) | tid)];
-            if (L.mix) rx_local3(a, L.c, L.s);
-            double2* st = S.state + base;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) st[(j << 9) | tid] = a[j];
-        }
-        __syncthreads();  // stage and LUT are refilled by the next iteration
-    }
-}
-
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass_high_p(const SlotDesc* __restrict__ slots,
-                                                               const LayerParam* __restrict__ lp,
-                                                               int layer, int Q, HighPass hp,
-                                                               uint32_t flags,
-                                                               uint32_t total_tiles) {
-    extern __shared__ __align__(16) double2 hbuf[];  // [2][4096]
-    const int tshift = Q - 12;
-    const uint32_t tmask = (1u << tshift) - 1u;
-    const bool fout = flags & F_EXPECT;
-    const bool sout = !fout || (flags & F_STATE_OUT);
-    const uint32_t tid = threadIdx.x;
-    const uint32_t w = tid & 7u;
-    const uint32_t tb = tid >> 3;
-    const int mp = hp.mpos;
-    auto mbit = [&](uint32_t tilebits) { return mp >= 0 && ((tilebits >> mp) & 1u); };
-    const uint32_t t_hi = tile_xor(hp, tb << 3);  // round-0 thread bits
-    const uint32_t t_r2 = tile_xor(hp, tb);       // round-2 thread bits
-    auto issue = [&](uint32_t t, int stage) {
-        if (t < total_tiles) {
-            const SlotDesc& S = slots[t >> tshift];
-            const LayerParam& L = lp[S.layer_base + layer];
-            if (L.mix || fout) {
-                const uint32_t g0 = (deposit(t & tmask, hp.freemask) | w) ^ t_hi;
-                double2* dst = hbuf + stage * 4096;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    cpa16(dst + (w | (j << 3) | (tb << 6)), S.state + (g0 ^ tile_xor(hp, static_cast<uint32_t>(j))));
-            }
-        }
-        cpa_commit();
-    };
-    uint32_t t = blockIdx.x;
-    issue(t, 0);
-    for (int k = 0; t < total_tiles; ++k, t += gridDim.x) {
-        const int stage = k & 1;
-        issue(t + gridDim.x, stage ^ 1);
-        const SlotDesc S = slots[t >> tshift];
-        const LayerParam L = lp[S.layer_base + layer];
-        const bool active = L.mix || fout;
-        const bool mix = L.mix;
-        const uint32_t x = deposit(t & tmask, hp.freemask) | w;
-        const uint32_t g2 = x ^ t_r2;
-        uint32_t lv[8];
-        if (active && fout) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
-                lv[j] = S.lev ? S.lev[g] : 0u;
-            }
-        }
-        cpa_wait1();  // own copies of this tile have landed (round 0 reads only those)
-        if (active) {
-            double2* sm = hbuf + stage * 4096;
-            double2 a[8];
-            {
-                const uint32_t tbits = tb << 3;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = sm[w | (j << 3) | (tb << 6)];
-                if (mix) high_round<0>(a, hp, mbit(tbits), L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) sm[w | (j << 3) | (tb << 6)] = a[j];
-            }
-            __syncthreads();
-            {
-                const uint32_t tbits = (tb & 7u) | ((tb >> 3) << 6);
-                const uint32_t e0 = w | ((tb & 7u) << 3) | ((tb >> 3) << 9);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = sm[e0 | (j << 6)];
-                if (mix) high_round<3>(a, hp, mbit(tbits), L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) sm[e0 | (j << 6)] = a[j];
-            }
-            __syncthreads();
-            {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) a[j] = sm[w | (tb << 3) | (j << 9)];
-                if (mix) high_round<6>(a, hp, mbit(tb), L.c, L.s);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
-                    if (sout) S.state[g] = a[j];
-                    if (fout)
-                        S.fbuf[g] = __dmul_rn(norm_rn(a[j]),
-                                              S.lev ? static_cast<double>(lv[j]) : (S.val ? S.val[g] : 1.0));
-                }
-            }
-        }
-        __syncthreads();  // the stage is refilled by the next iteration's prefetch
-    }
-}
-
-// ---------------------------------------------------------------------------
 // blocked expectation over f (statevector.hpp:48-65). Every 4096-block partial is a
 // chain of 4096 dependent adds (8.3-cycle DADD latency on B200 => >= 17 us), so the
 // kernel maximises concurrent chains: each LANE owns one chain. A warp covers up to 32
@@ -892,27 +689,18 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         QC_CUDA(cudaGetLastError());
         return 1;
     }
+    // (A persistent one-CTA-per-SM variant with a two-stage cp.async ring measured slower
+    // on B200: pass A 141 us / pass B 125 us vs 103 / 95 us for these 2-CTA/SM kernels.)
     static bool attrs = false;
-    static bool persist = false;
-    static int sms = 148;
     if (!attrs) {
         QC_CUDA(cudaFuncSetAttribute(k_pass_low, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kPassSmem)));
         QC_CUDA(cudaFuncSetAttribute(k_pass_high, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(4096 * sizeof(double2))));
-        QC_CUDA(cudaFuncSetAttribute(k_pass_low_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kPersistLowSmem)));
-        QC_CUDA(cudaFuncSetAttribute(k_pass_high_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(2 * 4096 * sizeof(double2))));
-        int dev = 0;
-        QC_CUDA(cudaGetDevice(&dev));
-        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (const char* env = std::getenv("QCG_PERSIST")) persist = std::strtol(env, nullptr, 10) != 0;
         attrs = true;
     }
     int launches = 0;
     const unsigned grid = static_cast<unsigned>(n_slots) << (Q - 12);
-    const unsigned pgrid = std::min<unsigned>(grid, static_cast<unsigned>(sms));
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
@@ -921,10 +709,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int active = fa ? n_slots : std::max(nph, nmix);
         const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream);
-        if (persist)
-            k_pass_low_p<<<pgrid, kPassThreads, kPersistLowSmem, stream>>>(d_slots, d_lp, l, Q, fa, grid);
-        else
-            k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
+        k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -938,12 +723,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             else
                 bh = nmix * 32.0 * N;
             if (prof) prof->begin(K_PASS_HIGH, bh, stream);
-            if (persist)
-                k_pass_high_p<<<pgrid, kPassThreads, 2 * 4096 * sizeof(double2), stream>>>(
-                    d_slots, d_lp, l, Q, plan.high[h], fh, grid);
-            else
-                k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
-                    d_slots, d_lp, l, Q, plan.high[h], fh);
+            k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
+                d_slots, d_lp, l, Q, plan.high[h], fh);
             if (prof) prof->end(stream);
             ++launches;
         }
