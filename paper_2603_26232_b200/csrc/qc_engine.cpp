@@ -415,26 +415,35 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                                      F_INIT | F_EXPECT, c * per, ctx(c));
             };
             for (size_t c = 0; c < nchunks; ++c) launch(c);
-            bool any = true;
-            while (any) {
-                any = false;
-                for (size_t c = 0; c < nchunks; ++c) {
-                    if (!inflight[c]) continue;
-                    vals.assign(pts[c].size(), 0.0);
-                    e->wait_chunk(ctx(c), vals.data());
-                    for (size_t k = 0; k < who[c].size(); ++k) {
-                        const size_t i = who[c][k];
-                        const double f = -vals[k];  // qaoa.hpp:90
-                        if (trace_x) {
-                            const auto& x = opt[i].point();
-                            (*trace_x)[i].insert((*trace_x)[i].end(), x.begin(), x.end());
-                            (*trace_f)[i].push_back(f);
-                        }
-                        opt[i].tell(f);
+            // completion-order service: whichever chunk's step finished is told/asked and
+            // re-enqueued first, so the device never idles behind a fixed host order
+            size_t live = 0;
+            for (size_t c = 0; c < nchunks; ++c) live += inflight[c] ? 1 : 0;
+            while (live) {
+                size_t c = nchunks;
+                for (;;) {
+                    for (size_t k = 0; k < nchunks && c == nchunks; ++k) {
+                        if (!inflight[k]) continue;
+                        const cudaError_t q = cudaEventQuery(ctx(k).done);
+                        if (q == cudaSuccess) c = k;
+                        else if (q != cudaErrorNotReady) QC_CUDA(q);
                     }
-                    launch(c);
-                    any = any || inflight[c];
+                    if (c != nchunks) break;
                 }
+                vals.assign(pts[c].size(), 0.0);
+                e->wait_chunk(ctx(c), vals.data());
+                for (size_t k = 0; k < who[c].size(); ++k) {
+                    const size_t i = who[c][k];
+                    const double f = -vals[k];  // qaoa.hpp:90
+                    if (trace_x) {
+                        const auto& x = opt[i].point();
+                        (*trace_x)[i].insert((*trace_x)[i].end(), x.begin(), x.end());
+                        (*trace_f)[i].push_back(f);
+                    }
+                    opt[i].tell(f);
+                }
+                launch(c);
+                if (!inflight[c]) --live;
             }
         }
     }
@@ -611,7 +620,15 @@ int qc_engine_create(int device, qc_engine** out) {
         auto* e = new qc_engine();
         e->device = device;
         QC_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-        for (auto& a : e->aux) QC_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+        // chunk streams with descending priority (main stream = chunk 0 = highest): when
+        // several chunks' kernels are runnable the device drains them in chunk order
+        int lo = 0, hi = 0;
+        QC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        QC_CUDA(cudaStreamDestroy(e->stream));
+        QC_CUDA(cudaStreamCreateWithPriority(&e->stream, cudaStreamNonBlocking, hi));
+        for (int k = 0; k < 3; ++k)
+            QC_CUDA(cudaStreamCreateWithPriority(&e->aux[k], cudaStreamNonBlocking,
+                                                 std::min(lo, hi + k + 1)));
         *out = e;
     });
 }
