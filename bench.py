@@ -50,8 +50,15 @@ WORKLOADS = {
     "c1": dict(n=100, p_edge=0.1, seed=0, qubit_cap=10, layers=1, top_k=4, budget=200,
                label="C1: ER(n=100,p=0.1,seed=0), cap 10 -> 11 x 10-qubit subgraphs, p=1, "
                      "top-K 4, level merge (8,388,608 leaves)"),
+    "c3": dict(n=1000, regular=3, wlo=1, whi=10, seed=0, qubit_cap=24, layers=1, top_k=2,
+               budget=200,
+               label="C3: weighted random 3-regular (n=1000, integer weights U{1..10}, seed 0), "
+                     "cap 24 -> 44 subgraphs (43 x 24 + 1 x 11 qubits), p=1, top-K 2"),
     "c4": dict(n=10000, p_edge=0.1, seed=0, qubit_cap=20, layers=1, top_k=2, budget=200,
                label="C4: ER(n=10000,p=0.1,seed=0), cap 20 -> 527 x 20-qubit subgraphs, p=1, "
+                     "top-K 2, windowed merge"),
+    "c5": dict(n=16000, p_edge=0.1, seed=0, qubit_cap=26, layers=1, top_k=2, budget=200,
+               label="C5: ER(n=16000,p=0.1,seed=0), cap 26 -> 640 x 26-qubit subgraphs, p=1, "
                      "top-K 2, windowed merge"),
 }
 
@@ -65,13 +72,21 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def er_graph(n, p, seed):
-    """ER(n, p, seed) exactly as graph.hpp:146-160 (mt19937_64, 53-bit draws)."""
-    from oracle.refpy import OracleLib, RefLib, ref_available, oracle_available
-    lib = RefLib() if ref_available() else (OracleLib() if oracle_available() else None)
-    if lib is None:
-        raise RuntimeError("no graph generator available (build oracle/)")
-    return lib.generate_er(n, p, seed)
+def workload_graph(w, reference=False):
+    """The workload's synthetic graph. The product arm uses the product's host generators
+    (qc_generate_er = graph.hpp:146-160; qc_generate_regular for config 3); the reference
+    arm uses the reference's own generator (oracle/_ref) — the graphs are identical
+    (tests/test_cpu_abi.py)."""
+    if reference:
+        from oracle.refpy import OracleLib, RefLib, ref_available
+        lib = RefLib() if ref_available() else OracleLib()
+        if "regular" in w:
+            return OracleLib().generate_regular(w["n"], w["regular"], w["seed"], w["wlo"], w["whi"])
+        return lib.generate_er(w["n"], w["p_edge"], w["seed"])
+    from paper_2603_26232_b200 import generate_er, generate_regular
+    if "regular" in w:
+        return generate_regular(w["n"], w["regular"], w["seed"], w["wlo"], w["whi"])
+    return generate_er(w["n"], w["p_edge"], w["seed"])
 
 
 class ClockSampler:
@@ -170,7 +185,7 @@ def run_reference_arm(args, w):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    edges = er_graph(w["n"], w["p_edge"], w["seed"])
+    edges = workload_graph(w, reference=True)
     for _ in range(args.warmup):
         reference_sample(w, edges)
     vals, totals = [], []
@@ -185,7 +200,7 @@ def run_reference_arm(args, w):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(totals) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w["label"], "n": w["n"], "p_edge": w["p_edge"],
+        "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
                    "qubit_cap": w["qubit_cap"], "layers": w["layers"], "top_k": w["top_k"],
                    "budget": w["budget"], "parallelism": f"cpu x{cores} threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
@@ -226,7 +241,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = Engine(local)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
-    edges = er_graph(w["n"], w["p_edge"], w["seed"])
+    edges = workload_graph(w)
     cfg = dict(qubit_cap=w["qubit_cap"], top_k=w["top_k"], layers=w["layers"],
                budget=w["budget"], seed=0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
@@ -377,8 +392,8 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (ER graph from the reference generator, graph.hpp:146)",
-        "config": {"workload": w["label"], "n": w["n"], "p_edge": w["p_edge"],
+        "data": "synthetic (graph.hpp:146 ER generator restated in qc_generate_er)",
+        "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
                    "qubit_cap": w["qubit_cap"], "subgraphs": n_sub, "layers": w["layers"],
                    "top_k": w["top_k"], "budget": w["budget"], "parallelism": f"shard{world}",
                    "l2": "working set (21 half-states x 8 MiB + f buffers) > 126 MB L2; "
@@ -390,7 +405,7 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            v, desc, kind, cores, _, total = reference_sample(w, edges)
+            v, desc, kind, cores, _, total = reference_sample(w, workload_graph(w, reference=True))
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
                                     "sample": desc}
         except Exception as ex:  # report, never fail the bench line

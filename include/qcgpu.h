@@ -180,6 +180,19 @@ int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h);
 /* The engine's cudaStream_t (all engine work is ordered on it). */
 void* qc_engine_stream(const qc_engine* e);
 
+/* ---- graph generators (host; instance prep, not timed by the reference) -------- */
+/* graph.hpp:146-160 generate_er_graph: pairs (u<v) in lex order, one mt19937_64 draw
+ * each, x = (draw >> 11) * 2^-53, edge iff x < p, weight 1. Two-call protocol: with
+ * edges == NULL only *m is written. */
+int qc_generate_er(int n, double p, uint64_t seed, qc_edge* edges, int64_t cap, int64_t* m);
+/* Weighted random d-regular graph (BASELINE config 3; the reference has no generator):
+ * configuration model over n*d stubs shuffled by Fisher-Yates with mt19937_64(seed)
+ * (j = draw % (i+1)), consecutive stubs paired; a shuffle giving a self-loop or a
+ * multi-edge is discarded and the next one drawn from the same stream. Integer weights
+ * U{wlo..whi} (draw % span) in the same stream, edges sorted by (u, v). */
+int qc_generate_regular(int n, int d, uint64_t seed, int wlo, int whi, qc_edge* edges,
+                        int64_t cap, int64_t* m);
+
 /* ---- statevector.hpp ---------------------------------------------------------- */
 /* statevector.hpp:75-111 CostTable: out[z] = C(z) for z < 2^n. */
 int qc_cost_table(qc_engine* e, const qc_graph* g, int cap, double* out, int* integral,

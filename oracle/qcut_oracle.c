@@ -171,6 +171,76 @@ int orc_generate_er(int n, double p, uint64_t seed, orc_edge* out, long long cap
     return 0;
 }
 
+/* Weighted random d-regular graph for BASELINE config 3 (the reference has no generator):
+ * configuration model, Fisher-Yates shuffle of n*d stubs with mt19937_64(seed)
+ * (j = draw % (i+1)), consecutive pairs; shuffles with a loop or multi-edge are
+ * discarded; then integer weights wlo + draw % span in (u, v)-sorted edge order. */
+static int cmp_edge_uv(const void* a, const void* b) {
+    const orc_edge* x = (const orc_edge*)a;
+    const orc_edge* y = (const orc_edge*)b;
+    if (x->u != y->u) return x->u < y->u ? -1 : 1;
+    return x->v < y->v ? -1 : (x->v > y->v);
+}
+
+int orc_generate_regular(int n, int d, uint64_t seed, int wlo, int whi, orc_edge* out,
+                         long long cap, long long* m) {
+    if (n < 1 || d < 1 || d >= n) return set_err(1, "regular graph needs 1 <= d < n");
+    if (((long long)n * d) % 2) return set_err(1, "n*d must be even");
+    if (wlo < 0 || whi < wlo) return set_err(1, "weight range must satisfy 0 <= wlo <= whi");
+    mt64 r;
+    mt64_seed(&r, seed);
+    size_t S = (size_t)n * (size_t)d, E = S / 2;
+    uint32_t* stubs = (uint32_t*)malloc(sizeof(uint32_t) * S);
+    orc_edge* es = (orc_edge*)malloc(sizeof(orc_edge) * (E ? E : 1));
+    uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (E ? E : 1));
+    for (int attempt = 0; attempt < 100000; ++attempt) {
+        for (size_t i = 0; i < S; ++i) stubs[i] = (uint32_t)(i / (size_t)d);
+        for (size_t i = S - 1; i > 0; --i) {
+            size_t j = (size_t)(mt64_next(&r) % (uint64_t)(i + 1));
+            uint32_t t = stubs[i];
+            stubs[i] = stubs[j];
+            stubs[j] = t;
+        }
+        int ok = 1;
+        for (size_t k = 0; k < E && ok; ++k) {
+            uint32_t u = stubs[2 * k], v = stubs[2 * k + 1];
+            if (u == v) ok = 0;
+            if (u > v) {
+                uint32_t t = u;
+                u = v;
+                v = t;
+            }
+            es[k].u = u;
+            es[k].v = v;
+            es[k].w = 0.0;
+            keys[k] = (uint64_t)u * (uint64_t)n + v;
+        }
+        if (ok) { /* multi-edge check (the product checks in pairing order; same verdict) */
+            qsort(keys, E, sizeof(uint64_t), cmp_u64);
+            for (size_t k = 1; k < E; ++k)
+                if (keys[k] == keys[k - 1]) ok = 0;
+        }
+        if (!ok) continue;
+        qsort(es, E, sizeof(orc_edge), cmp_edge_uv);
+        uint64_t span = (uint64_t)(whi - wlo + 1);
+        for (size_t k = 0; k < E; ++k) es[k].w = (double)(wlo + (int)(mt64_next(&r) % span));
+        *m = (long long)E;
+        int rc = 0;
+        if (out) {
+            if (cap < (long long)E) rc = set_err(1, "edge buffer too small");
+            else memcpy(out, es, sizeof(orc_edge) * E);
+        }
+        free(stubs);
+        free(es);
+        free(keys);
+        return rc;
+    }
+    free(stubs);
+    free(es);
+    free(keys);
+    return set_err(2, "no simple regular graph found");
+}
+
 /* ------------------------------------------------------------------------ */
 /* partition.hpp                                                             */
 /* ------------------------------------------------------------------------ */

@@ -48,6 +48,8 @@ int orc_qubit_cap(void);
 void orc_set_qubit_cap(int cap); /* kQubitCap, statevector.hpp:20 (24; 26 for config 5) */
 
 int orc_generate_er(int n, double p, uint64_t seed, orc_edge* out, long long cap, long long* m);
+int orc_generate_regular(int n, int d, uint64_t seed, int wlo, int whi, orc_edge* out,
+                         long long cap, long long* m);
 int orc_partition(int n, int m, const orc_edge* e, int M, int mode, int cap, int* first, int* last,
                   int* local_m, long long* inter_m);
 int orc_derive_subgraph_count(long long n, long long cap, int* out);

@@ -326,6 +326,15 @@ class OracleLib(_Lib):
     def __init__(self):
         super().__init__(ORACLE_SO)
 
+    def generate_regular(self, n: int, d: int, seed: int, wlo: int = 1, whi: int = 10) -> np.ndarray:
+        m = C.c_longlong(0)
+        self._call("generate_regular", C.c_int(n), C.c_int(d), C.c_uint64(seed), C.c_int(wlo),
+                   C.c_int(whi), None, C.c_longlong(0), C.byref(m))
+        out = np.zeros(m.value, dtype=EDGE_DTYPE)
+        self._call("generate_regular", C.c_int(n), C.c_int(d), C.c_uint64(seed), C.c_int(wlo),
+                   C.c_int(whi), _p(out), C.c_longlong(m.value), C.byref(m))
+        return out
+
     def set_qubit_cap(self, cap: int):
         """kQubitCap (statevector.hpp:20): 24 in the reference, 26 for config 5."""
         self.lib.orc_set_qubit_cap(C.c_int(cap))

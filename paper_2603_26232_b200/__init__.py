@@ -124,7 +124,8 @@ EXPORTED_SYMBOLS = [
     "qc_engine_transfers", "qc_engine_stream", "qc_pipeline_prepare", "qc_pipeline_execute",
     "qc_pipeline_destroy", "qc_simplex_create", "qc_simplex_ask", "qc_simplex_tell",
     "qc_simplex_result", "qc_simplex_destroy", "qc_optimizer_create", "qc_optimizer_ask",
-    "qc_optimizer_tell", "qc_optimizer_result", "qc_optimizer_destroy",
+    "qc_optimizer_tell", "qc_optimizer_result", "qc_optimizer_destroy", "qc_generate_er",
+    "qc_generate_regular",
 ]
 
 KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
@@ -216,6 +217,30 @@ class Partition:  # partition.hpp:22-34 (chain pieces as global id ranges)
     last: np.ndarray
     local: list = field(default_factory=list)  # (n_local, EDGE_DTYPE array in local ids)
     inter: int = 0
+
+
+def generate_er(n: int, p: float, seed: int) -> np.ndarray:
+    """graph.hpp:146-160 generate_er_graph (host, qc_generate_er)."""
+    lib = load_library()
+    m = C.c_int64(0)
+    _check(lib, lib.qc_generate_er(C.c_int(n), C.c_double(p), C.c_uint64(seed), None,
+                                   C.c_int64(0), C.byref(m)))
+    out = np.zeros(m.value, dtype=EDGE_DTYPE)
+    _check(lib, lib.qc_generate_er(C.c_int(n), C.c_double(p), C.c_uint64(seed), _p(out),
+                                   C.c_int64(m.value), C.byref(m)))
+    return out
+
+
+def generate_regular(n: int, d: int, seed: int, wlo: int = 1, whi: int = 10) -> np.ndarray:
+    """Weighted random d-regular graph, integer weights U{wlo..whi} (BASELINE config 3)."""
+    lib = load_library()
+    m = C.c_int64(0)
+    _check(lib, lib.qc_generate_regular(C.c_int(n), C.c_int(d), C.c_uint64(seed), C.c_int(wlo),
+                                        C.c_int(whi), None, C.c_int64(0), C.byref(m)))
+    out = np.zeros(m.value, dtype=EDGE_DTYPE)
+    _check(lib, lib.qc_generate_regular(C.c_int(n), C.c_int(d), C.c_uint64(seed), C.c_int(wlo),
+                                        C.c_int(whi), _p(out), C.c_int64(m.value), C.byref(m)))
+    return out
 
 
 def derive_subgraph_count(n: int, cap: int) -> int:  # partition.hpp:163-167

@@ -7,6 +7,7 @@
 #include <memory>
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -360,9 +361,76 @@ void write_assignment(const std::vector<uint8_t>& a, char* out) {
     out[a.size()] = 0;
 }
 
+
+// graph.hpp:146-160 and the config-3 regular generator (host instance prep)
+std::vector<qc_edge_t> gen_er(int n, double p, uint64_t seed) {
+    if (p < 0.0 || p > 1.0 || std::isnan(p)) config_error("edge probability must lie in [0,1]");
+    if (n < 0) config_error("negative vertex count");
+    std::vector<qc_edge_t> out;
+    std::mt19937_64 rng(seed);
+    for (uint32_t u = 0; u + 1 < static_cast<uint32_t>(n); ++u)
+        for (uint32_t v = u + 1; v < static_cast<uint32_t>(n); ++v) {
+            const double x = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+            if (x < p) out.push_back({u, v, 1.0});
+        }
+    return out;
+}
+
+std::vector<qc_edge_t> gen_regular(int n, int d, uint64_t seed, int wlo, int whi) {
+    if (n < 1 || d < 1 || d >= n) config_error("regular graph needs 1 <= d < n");
+    if ((static_cast<long long>(n) * d) % 2) config_error("n*d must be even");
+    if (wlo < 0 || whi < wlo) config_error("weight range must satisfy 0 <= wlo <= whi");
+    std::mt19937_64 rng(seed);
+    const size_t S = static_cast<size_t>(n) * static_cast<size_t>(d);
+    std::vector<uint32_t> stubs(S);
+    std::vector<qc_edge_t> out;
+    for (int attempt = 0; attempt < 100000; ++attempt) {
+        for (size_t i = 0; i < S; ++i) stubs[i] = static_cast<uint32_t>(i / static_cast<size_t>(d));
+        for (size_t i = S - 1; i > 0; --i) {
+            const size_t j = static_cast<size_t>(rng() % (i + 1));
+            std::swap(stubs[i], stubs[j]);
+        }
+        out.clear();
+        std::unordered_set<uint64_t> seen;
+        bool ok = true;
+        for (size_t i = 0; i < S && ok; i += 2) {
+            uint32_t u = stubs[i], v = stubs[i + 1];
+            if (u == v) ok = false;
+            if (u > v) std::swap(u, v);
+            if (ok && !seen.insert(static_cast<uint64_t>(u) * static_cast<uint64_t>(n) + v).second) ok = false;
+            if (ok) out.push_back({u, v, 0.0});
+        }
+        if (!ok) continue;
+        std::sort(out.begin(), out.end(), [](const qc_edge_t& a, const qc_edge_t& b) {
+            return a.u != b.u ? a.u < b.u : a.v < b.v;
+        });
+        const uint64_t span = static_cast<uint64_t>(whi - wlo + 1);
+        for (auto& e : out) e.w = static_cast<double>(wlo + static_cast<int>(rng() % span));
+        return out;
+    }
+    resource_error("no simple regular graph found");
+}
+
+int copy_edges(const std::vector<qc_edge_t>& g, qc_edge* edges, int64_t cap, int64_t* m) {
+    *m = static_cast<int64_t>(g.size());
+    if (!edges) return 0;
+    if (cap < *m) config_error("edge buffer too small");
+    std::memcpy(edges, g.data(), g.size() * sizeof(qc_edge_t));
+    return 0;
+}
+
 }  // namespace
 
 extern "C" {
+
+int qc_generate_er(int n, double p, uint64_t seed, qc_edge* edges, int64_t cap, int64_t* m) {
+    return guarded([&] { copy_edges(gen_er(n, p, seed), edges, cap, m); });
+}
+
+int qc_generate_regular(int n, int d, uint64_t seed, int wlo, int whi, qc_edge* edges,
+                        int64_t cap, int64_t* m) {
+    return guarded([&] { copy_edges(gen_regular(n, d, seed, wlo, whi), edges, cap, m); });
+}
 
 int qc_level_merge(qc_engine* e, const qc_pool* pool, const qc_graph* g, const qc_chain* chain,
                    const qc_merge_options* opt, qc_merge_result* res) {

@@ -168,3 +168,17 @@ def test_python_partition_mirror_matches_oracle(oracle):
         assert [len(x[1]) for x in P.local] == list(lm)
     assert derive_subgraph_count(100, 10) == oracle.derive_subgraph_count(100, 10) == 11
     assert derive_subgraph_count(16000, 26) == 640 and derive_subgraph_count(10000, 20) == 527
+
+
+def test_product_generators_match_oracle(oracle):
+    """bench.py builds its inputs with the PRODUCT's host generators (qc_generate_er,
+    graph.hpp:146-160; qc_generate_regular for config 3); they equal the oracle's."""
+    from paper_2603_26232_b200 import generate_er, generate_regular
+    for n, p, seed in [(100, 0.1, 0), (400, 0.1, 0), (37, 0.5, 9)]:
+        assert np.array_equal(generate_er(n, p, seed), oracle.generate_er(n, p, seed))
+    g = generate_regular(1000, 3, 0, 1, 10)
+    assert np.array_equal(g, oracle.generate_regular(1000, 3, 0, 1, 10))
+    assert len(g) == 1500
+    deg = np.bincount(np.concatenate([g["u"], g["v"]]), minlength=1000)
+    assert (deg == 3).all() and (g["u"] < g["v"]).all()
+    assert set(np.unique(g["w"])) <= set(float(x) for x in range(1, 11))
