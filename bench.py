@@ -293,9 +293,11 @@ def main():
         step_value()
         barrier()
     clocks = ClockSampler(local)
+    eng.host_stats(reset=True)
     clocks.start()
     t_val, rep, launches, profile = timed(step_value, args.steps, prof=True)
     clk = clocks.stop()
+    host = eng.host_stats(reset=True)
 
     # max over ranks
     tot = torch.tensor([sum(t_val)], dtype=torch.float64, device=f"cuda:{local}")
@@ -400,6 +402,8 @@ def main():
                          "L2 flushed (256 MB write) between timed steps"},
         "solve_time_s": sec_per_step, "cut": rep.cut, "evals_per_step": evals_per_step,
         "step_ms": [round(t * 1e3, 2) for t in t_val],
+        "host_s_per_step": {k: (v / args.steps if k != "chunk_steps" else v // args.steps)
+                            for k, v in host.items()},
         "stage_s": {"partition": rep.partition_s, "qaoa": rep.qaoa_s, "merge": rep.merge_s},
         "e2e": e2e, "gpu_launches": int(lt.item()), "clocks": clk, "roofline": roofline,
     }

@@ -175,6 +175,10 @@ int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
 int qc_engine_profile(qc_engine* e, int on);
 int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
                            double* bytes);
+/* Host time of the lockstep optimiser: waiting for chunk results vs preparing the next
+ * step (NM tell/ask, phase LUTs, staging, launches), and chunk-steps serviced. */
+int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t* steps,
+                         int reset);
 /* Host<->device bytes copied by this engine since creation. */
 int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h);
 /* The engine's cudaStream_t (all engine work is ordered on it). */

@@ -5,6 +5,7 @@
 #include "qc_engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -419,8 +420,10 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             // re-enqueued first, so the device never idles behind a fixed host order
             size_t live = 0;
             for (size_t c = 0; c < nchunks; ++c) live += inflight[c] ? 1 : 0;
+            using clk = std::chrono::steady_clock;
             while (live) {
                 size_t c = nchunks;
+                const auto tw = clk::now();
                 for (;;) {
                     for (size_t k = 0; k < nchunks && c == nchunks; ++k) {
                         if (!inflight[k]) continue;
@@ -430,6 +433,8 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                     }
                     if (c != nchunks) break;
                 }
+                const auto tp = clk::now();
+                e->host_wait_s += std::chrono::duration<double>(tp - tw).count();
                 vals.assign(pts[c].size(), 0.0);
                 e->wait_chunk(ctx(c), vals.data());
                 for (size_t k = 0; k < who[c].size(); ++k) {
@@ -443,6 +448,8 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                     opt[i].tell(f);
                 }
                 launch(c);
+                e->host_prep_s += std::chrono::duration<double>(clk::now() - tp).count();
+                ++e->host_steps;
                 if (!inflight[c]) --live;
             }
         }
@@ -663,6 +670,20 @@ int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* m
         if (launches) *launches = e->prof.count[kind];
         if (ms) *ms = e->prof.ms[kind];
         if (bytes) *bytes = e->prof.bytes[kind];
+    });
+}
+
+int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t* steps,
+                         int reset) {
+    return guarded([&] {
+        if (!e) config_error("null engine");
+        if (wait_s) *wait_s = e->host_wait_s;
+        if (prep_s) *prep_s = e->host_prep_s;
+        if (steps) *steps = e->host_steps;
+        if (reset) {
+            e->host_wait_s = e->host_prep_s = 0.0;
+            e->host_steps = 0;
+        }
     });
 }
 
