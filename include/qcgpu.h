@@ -179,6 +179,9 @@ int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* m
  * step (NM tell/ask, phase LUTs, staging, launches), and chunk-steps serviced. */
 int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t* steps,
                          int reset);
+/* Host wall seconds accumulated since the last host_stats reset: [0] lockstep optimise,
+ * [1] final circuits + top-K, [2] merge, [3] whole qc_pipeline_execute. */
+int qc_engine_phase_times(const qc_engine* e, double* out4);
 /* Host<->device bytes copied by this engine since creation. */
 int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h);
 /* The engine's cudaStream_t (all engine work is ordered on it). */

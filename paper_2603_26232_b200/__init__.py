@@ -125,7 +125,7 @@ EXPORTED_SYMBOLS = [
     "qc_pipeline_destroy", "qc_simplex_create", "qc_simplex_ask", "qc_simplex_tell",
     "qc_simplex_result", "qc_simplex_destroy", "qc_optimizer_create", "qc_optimizer_ask",
     "qc_optimizer_tell", "qc_optimizer_result", "qc_optimizer_destroy", "qc_generate_er",
-    "qc_generate_regular", "qc_engine_host_stats",
+    "qc_generate_regular", "qc_engine_host_stats", "qc_engine_phase_times",
 ]
 
 KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
@@ -359,9 +359,12 @@ class Engine:
 
     def host_stats(self, reset: bool = False):
         w, p_, n = C.c_double(0), C.c_double(0), C.c_uint64(0)
+        ph = (C.c_double * 4)()
+        _check(self.lib, self.lib.qc_engine_phase_times(self._h, ph))
         _check(self.lib, self.lib.qc_engine_host_stats(self._h, C.byref(w), C.byref(p_), C.byref(n),
                                                        C.c_int(int(reset))))
-        return dict(wait_s=w.value, prep_s=p_.value, chunk_steps=int(n.value))
+        return dict(wait_s=w.value, prep_s=p_.value, chunk_steps=int(n.value),
+                    optimize_s=ph[0], final_s=ph[1], merge_s=ph[2], execute_s=ph[3])
 
     def transfers(self):
         h = C.c_uint64(0)

@@ -501,7 +501,15 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
         seeds[i] = opts[i].seed;
         tol[i] = opts[i].tolerance;
     }
+    const auto t0 = std::chrono::steady_clock::now();
     const auto best = optimize_batch(e, dg, layers, budget, seeds, tol, nullptr, nullptr);
+    const auto t1 = std::chrono::steady_clock::now();
+    e->t_optimize_s += std::chrono::duration<double>(t1 - t0).count();
+    struct FinalTimer {
+        qc_engine* e;
+        std::chrono::steady_clock::time_point t;
+        ~FinalTimer() { e->t_final_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
+    } final_timer{e, t1};
 
     // final circuit at the best angles (qaoa.hpp:208) + top-K (qaoa.hpp:211)
     std::vector<SolveOut> out(n);
@@ -683,7 +691,18 @@ int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t*
         if (reset) {
             e->host_wait_s = e->host_prep_s = 0.0;
             e->host_steps = 0;
+            e->t_optimize_s = e->t_final_s = e->t_merge_s = e->t_execute_s = 0.0;
         }
+    });
+}
+
+int qc_engine_phase_times(const qc_engine* e, double* out4) {
+    return guarded([&] {
+        if (!e) config_error("null engine");
+        out4[0] = e->t_optimize_s;
+        out4[1] = e->t_final_s;
+        out4[2] = e->t_merge_s;
+        out4[3] = e->t_execute_s;
     });
 }
 

@@ -88,6 +88,7 @@ struct qc_engine {
     uint64_t h2d = 0, d2h = 0;  // bytes copied host<->device by this engine
     double host_wait_s = 0.0, host_prep_s = 0.0;  // lockstep loop: waiting vs preparing
     uint64_t host_steps = 0;
+    double t_optimize_s = 0.0, t_final_s = 0.0, t_merge_s = 0.0, t_execute_s = 0.0;
 
     // Build the device cut tables of graphs (sym: half state) into `target` (default:
     // the engine's shared `tables` buffer, valid until the next prepare()).

@@ -572,6 +572,8 @@ int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment
         bool windowed = false;
         const MergeOutput out = merge_stage(e, pl->g, pl->P, solves, &pl->cfg, &windowed);
         r.merge_s = seconds_since(t0);
+        e->t_merge_s += r.merge_s;
+        e->t_execute_s += r.qaoa_s + r.merge_s;
         r.total_s = r.partition_s + r.qaoa_s + r.merge_s;
         r.cut = out.value;
         r.candidates_evaluated = out.leaves;
