@@ -169,6 +169,11 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                  unsigned* d_tickets, double* d_out, cudaStream_t stream,
                  const ChainStats* stats = nullptr, Prof* prof = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
+// v4 streaming passes (qc_pass.cu): persistent, one CTA per SM
+int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
+                   int n_slots, cudaStream_t stream);
+int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
+                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream);
 
 // Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,
 // ordered by (prob desc, lex asc) (qaoa.hpp:179-182). d_scratch sized by topk_scratch_bytes.

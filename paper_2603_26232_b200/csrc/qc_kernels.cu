@@ -701,6 +701,10 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     }
     int launches = 0;
     const unsigned grid = static_cast<unsigned>(n_slots) << (Q - 12);
+    static const bool v3 = [] {
+        const char* e = std::getenv("QCG_PASS");
+        return e && std::atoi(e) == 3;
+    }();
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
@@ -709,7 +713,10 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int active = fa ? n_slots : std::max(nph, nmix);
         const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream);
-        k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
+        if (v3)
+            k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
+        else
+            launch_pass_a4(d_slots, d_lp, l, Q, fa, n_slots, stream);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -723,8 +730,11 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             else
                 bh = nmix * 32.0 * N;
             if (prof) prof->begin(K_PASS_HIGH, bh, stream);
-            k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
-                d_slots, d_lp, l, Q, plan.high[h], fh);
+            if (v3)
+                k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
+                    d_slots, d_lp, l, Q, plan.high[h], fh);
+            else
+                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh, n_slots, stream);
             if (prof) prof->end(stream);
             ++launches;
         }

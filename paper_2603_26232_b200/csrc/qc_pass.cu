@@ -1,0 +1,577 @@
+// Streaming pass kernels v4 (sm_100a): persistent CTAs, two consumer groups per CTA and
+// a three-stage cp.async ring in shared memory.
+//
+// Why this shape. A pass moves every stored amplitude HBM -> SM -> HBM once and applies
+// 6 FP64 ops per amplitude per RX target (no FMA: statevector.hpp:176-180 is replayed
+// with explicit __dmul_rn/__dadd_rn). On B200 the per-SM share of HBM is ~23 B/clk, so a
+// 4096-amplitude tile (64 KB in + 64 KB out) costs ~5.7k clk of bandwidth, while pass A's
+// 78 FP64 ops/amp cost ~5.0k clk of the 64-lane FP64 pipe and the shared-memory rounds
+// ~3.5k clk. All three must overlap. v3 (one tile per CTA, 2 CTAs/SM) serialised "load ->
+// compute" inside each CTA and left HBM idle whenever both CTAs computed. Here:
+//   * loads of tiles k+1, k+2 are in flight (cp.async -> mbarrier) while tile k computes;
+//   * two 256-thread groups work on alternate tiles, so one group's FP64 rounds overlap
+//     the other's shared-memory traffic (group-local named barriers, no CTA barrier);
+//   * 16 amplitudes per thread: 4 targets per register round, 3 rounds for 12 bits
+//     (v3: 8 amps, 4 rounds), i.e. fewer shared-memory round trips per tile.
+//
+// Ring protocol. Local tile k of a CTA lives in stage k % 3 and is computed by group
+// k % 2. The group that finishes reading tile k from its stage immediately refills the
+// stage with tile k + 3 (which the OTHER group computes). Each stage has a "full"
+// mbarrier (256 arrivals: every issuing thread's cp.async.mbarrier.arrive.noinc) and a
+// tag word = the local tile index it was last filled with; a consumer first waits for the
+// tag (so it never tests the parity of a phase two generations ahead), then the parity.
+//
+// Exactness is unchanged from v3: per amplitude the phase precedes RX targets in
+// ascending order, the mirror op (RX on qubit q-1 in half-state storage) comes last, and
+// mixer_pair is bitwise symmetric in its two operands (IEEE add/mul commute), so the
+// order of a pair's roles is immaterial.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+#include "qc_internal.hpp"
+
+namespace qcg {
+namespace v4 {
+
+constexpr int kGT = 256;             // threads per consumer group
+constexpr int kThreads = 2 * kGT;    // two groups
+constexpr int kStages = 3;
+constexpr int kLutCap = 256;         // LUT entries kept per group in shared memory
+constexpr int kDescCap = 24;         // slot descriptors cached per CTA
+constexpr uint32_t kStageAmpBytes = 4096u * 16u;
+constexpr uint32_t kOffLev = kStages * kStageAmpBytes;             // levels per stage (8 KB)
+constexpr uint32_t kOffLut = kOffLev + kStages * 4096u * 2u;       // per-group LUT
+constexpr uint32_t kOffBar = kOffLut + 2u * kLutCap * 16u;         // full barriers
+constexpr uint32_t kOffTag = kOffBar + kStages * 8u;               // tags + per-stage words
+constexpr uint32_t kOffDesc = kOffTag + 32u;
+
+// Per-slot view of (SlotDesc, LayerParam[layer]) cached in shared memory at kernel start,
+// so a tile's first instructions do not wait on two dependent global loads.
+struct PD {
+    double2* state;
+    double* fbuf;
+    const uint16_t* lev;
+    const double* val;
+    const double2* lut;
+    double amp0, c, s, gamma;
+    int32_t phase, mix, lut_len, key;
+};
+constexpr uint32_t kSmem = kOffDesc + kDescCap * sizeof(PD);
+static_assert(kSmem <= 232448, "shared memory budget");
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t sw4(uint32_t e) { return e ^ ((e >> 4) & 7u); }
+
+__device__ __forceinline__ void cpa16(uint32_t s, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa_arrive(uint32_t bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void grp_sync(uint32_t g) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(g + 1u), "n"(kGT) : "memory");
+}
+
+// exact fp64 blocks (same as qc_kernels.cu)
+__device__ __forceinline__ double2 cmul(double2 a, double2 l) {
+    return make_double2(__dsub_rn(__dmul_rn(a.x, l.x), __dmul_rn(a.y, l.y)),
+                        __dadd_rn(__dmul_rn(a.x, l.y), __dmul_rn(a.y, l.x)));
+}
+__device__ __forceinline__ void rx(double2& a0, double2& a1, double c, double s) {
+    const double2 t0 = a0, t1 = a1;
+    a0.x = __dadd_rn(__dmul_rn(c, t0.x), __dmul_rn(s, t1.y));
+    a0.y = __dsub_rn(__dmul_rn(c, t0.y), __dmul_rn(s, t1.x));
+    a1.x = __dadd_rn(__dmul_rn(s, t0.y), __dmul_rn(c, t1.x));
+    a1.y = __dsub_rn(__dmul_rn(c, t1.y), __dmul_rn(s, t0.x));
+}
+__device__ __forceinline__ double nrm(double2 a) {
+    return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+}
+
+// fractional weights: std::polar(1, -gamma*val) (device sincos), out of line so the
+// integral path keeps its registers
+__device__ __noinline__ double2 phase_frac(double2 v, double gamma, double val) {
+    double sn, cs;
+    sincos(__dmul_rn(-gamma, val), &sn, &cs);
+    return cmul(v, make_double2(cs, sn));
+}
+
+// RX on local bits [B0, B0+NB) of a[16] (ascending)
+template <int B0, int NB>
+__device__ __forceinline__ void rx_local(double2 (&a)[16], double c, double s) {
+#pragma unroll
+    for (int b = B0; b < B0 + NB; ++b) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) rx(a[j], a[j | (1 << b)], c, s);
+    }
+}
+
+__device__ __forceinline__ void tile_range(uint32_t total, uint32_t& t0, int& cnt) {
+    const uint64_t b = blockIdx.x, G = gridDim.x;
+    t0 = static_cast<uint32_t>(b * total / G);
+    cnt = static_cast<int>(static_cast<uint32_t>((b + 1) * total / G) - t0);
+}
+
+// Slot range of this CTA's tiles -> descriptor cache (caller guarantees it fits).
+__device__ __forceinline__ void load_descs(PD* pd, const SlotDesc* __restrict__ slots,
+                                           const LayerParam* __restrict__ lp, int layer,
+                                           uint32_t sa, uint32_t n) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const SlotDesc S = slots[sa + i];
+        const LayerParam L = lp[S.layer_base + layer];
+        PD d;
+        d.state = S.state;
+        d.fbuf = S.fbuf;
+        d.lev = S.lev;
+        d.val = S.val;
+        d.lut = L.lut;
+        d.amp0 = S.amp0;
+        d.c = L.c;
+        d.s = L.s;
+        d.gamma = L.gamma;
+        d.phase = L.phase;
+        d.mix = L.mix;
+        d.lut_len = L.lut_len;
+        d.key = static_cast<int32_t>(sa + i);
+        pd[i] = d;
+    }
+}
+
+__device__ __forceinline__ void ring_init(unsigned char* sm) {
+    if (threadIdx.x < kStages) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(sm + kOffBar) + threadIdx.x * 8u),
+                     "r"(kGT)
+                     : "memory");
+        reinterpret_cast<volatile int*>(sm + kOffTag)[threadIdx.x] = -1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pass A: tile = 4096 contiguous stored amplitudes; [|+> init] + phase + RX 0..11.
+// Rounds: bits 0-3 (e = gt*16 + j), bits 4-7, bits 8-11 (e = j*256 + gt, coalesced store).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_a(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
+             int Q, uint32_t flags, uint32_t total_tiles) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
+    const int tshift = Q - 12;
+    const uint32_t tmask = (1u << tshift) - 1u;
+    const bool init = flags & F_INIT;
+    uint32_t t0;
+    int cnt;
+    tile_range(total_tiles, t0, cnt);
+    if (cnt <= 0) return;
+    const uint32_t sa = t0 >> tshift;
+    PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
+    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    ring_init(sm);
+    __syncthreads();
+    const uint32_t bar0 = su32(sm + kOffBar);
+    volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
+
+    // the calling group fills stage k%3 with local tile k
+    auto issue = [&](int k) {
+        if (k >= cnt) return;
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const uint32_t base = (t & tmask) << 12;
+        bool any = false;
+        if (init || d.phase || d.mix) {
+            if (!init) {
+                const uint32_t sb = su32(sm + s * kStageAmpBytes);
+                const double2* src = d.state + base + gt;
+                const uint32_t d0 = sb + sw4(gt) * 16u;  // sw4(gt + 256 i) = sw4(gt) + 256 i
+#pragma unroll
+                for (int i = 0; i < 16; ++i) cpa16(d0 + i * (kGT * 16u), src + kGT * i);
+                any = true;
+            }
+            if (d.phase && d.lev) {
+                const uint32_t lb = su32(sm + kOffLev + s * 8192u);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t u = gt + kGT * i;  // 16-byte unit = 8 levels
+                    cpa16(lb + u * 16u, d.lev + base + u * 8u);
+                }
+                any = true;
+            }
+        }
+        if (gt == 0) tag[s] = k;
+        if (any)
+            cpa_arrive(bar0 + s * 8u);
+        else
+            bar_arrive(bar0 + s * 8u);
+    };
+    if (g == 0) {
+        issue(0);
+        issue(2);
+    } else {
+        issue(1);
+    }
+
+    double2* slut = reinterpret_cast<double2*>(sm + kOffLut) + g * kLutCap;
+    int lut_owner = -1;  // slot whose LUT slut holds
+    for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool act = init || d.phase || d.mix;
+        const bool use_lev = d.phase && d.lev;
+        const bool lut_sm = use_lev && d.lut_len <= kLutCap;
+        if (lut_sm && lut_owner != d.key) {
+            // every thread of the group is past the previous tile's phase (round-0) reads
+            const double2* lsrc = d.lut;
+            for (int i = static_cast<int>(gt); i < d.lut_len; i += kGT) slut[i] = lsrc[i];
+            lut_owner = d.key;
+            grp_sync(g);
+        }
+        while (tag[s] != k) {
+        }
+        bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
+        if (!act) {
+            issue(k + kStages);
+            continue;  // identity layer: memory already holds the result
+        }
+        const uint32_t base = (t & tmask) << 12;
+        double2* st = reinterpret_cast<double2*>(sm + s * kStageAmpBytes);
+        const double c = d.c, sn = d.s;
+        const bool mix = d.mix;
+        double2 a[16];
+        // round 0: bits 0-3, phase first
+        {
+            const uint4* lv = reinterpret_cast<const uint4*>(sm + kOffLev + s * 8192u) + gt * 2u;
+            const double2* lutp = lut_sm ? slut : d.lut;
+            const bool phase = d.phase;
+            const double amp0 = d.amp0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = h * 8 + jj;
+                    const uint32_t e = gt * 16u + j;
+                    double2 v = init ? make_double2(amp0, 0.0) : st[sw4(e)];
+                    if (phase) {
+                        if (use_lev) {
+                            const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
+                                                : (jj >> 1) == 2 ? l4.z : l4.w;
+                            v = cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
+                        } else {
+                            v = phase_frac(v, d.gamma, d.val[base + e]);
+                        }
+                    }
+                    a[j] = v;
+                }
+            }
+            if (mix) rx_local<0, 4>(a, c, sn);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[sw4(gt * 16u + j)] = a[j];
+        }
+        grp_sync(g);
+        // round 1: bits 4-7, e = (gt>>4)<<8 | j<<4 | gt&15
+        {
+            const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = st[sw4(r | (j << 4))];
+            if (mix) rx_local<0, 4>(a, c, sn);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[sw4(r | (j << 4))] = a[j];
+        }
+        grp_sync(g);
+        // round 2: bits 8-11, e = j<<8 | gt
+        const double2* st2 = st + sw4(gt);  // sw4(j<<8 | gt) = j<<8 | sw4(gt)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st2[j << 8];
+        double2* __restrict__ dst = d.state + base;
+        grp_sync(g);  // the whole group is done with this stage: refill it
+        issue(k + kStages);
+        if (mix) rx_local<0, 4>(a, c, sn);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcs(dst + ((j << 8) | gt), a[j]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pass B: tile = 8 contiguous amps (column bits 0-2) x 9 gathered tile bits (RX targets
+// >= 12, then the mirror pseudo-bit whose mask is every stored bit, then no-op pads).
+// Tile index e = w | gb << 3 (gb: 9 gather bits); global index = x ^ hx(gb) where
+// x = deposit(tile, freemask) | w and hx() folds the gather-bit masks (kernel parameters:
+// the XORs of compile-time bit subsets compile to LOP3s on constant-bank operands).
+// Rounds: gather bits 0-3, 4-7, 8 (each only if it holds an op); the last round writes
+// the state and/or f(z) = |a|^2 C(z) straight from registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t hx(const HighPass& hp, uint32_t bits) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < kHighBits; ++b)
+        if ((bits >> b) & 1u) x ^= hp.mask[b];
+    return x;
+}
+
+__device__ __forceinline__ uint32_t deposit4(uint32_t v, uint32_t mask) {
+    uint32_t x = 0;
+    while (mask) {
+        const uint32_t low = mask & (~mask + 1u);
+        if (v & 1u) x |= low;
+        v >>= 1;
+        mask &= mask - 1u;
+    }
+    return x;
+}
+
+// pair ops on local bits of a[16]: local bit b -> gather bit G0 + b (kind != 0 => op)
+template <int G0, int NB>
+__device__ __forceinline__ void ops_local(double2 (&a)[16], const HighPass& hp, double c, double s) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        if (hp.kind[G0 + b] == 0) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) rx(a[j], a[j | (1 << b)], c, s);
+    }
+}
+
+// gather bits of amp j in round R (the j-dependent part; compile-time after unrolling)
+template <int R>
+__device__ __forceinline__ uint32_t gb_local(int j) {
+    if (R == 0) return static_cast<uint32_t>(j);
+    if (R == 1) return static_cast<uint32_t>(j) << 4;
+    return (static_cast<uint32_t>(j >> 1) & 7u) | (static_cast<uint32_t>(j & 1) << 8);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_b(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
+             int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
+    const int tshift = Q - 12;
+    const uint32_t tmask = (1u << tshift) - 1u;
+    const bool fout = flags & F_EXPECT;
+    const bool sout = !fout || (flags & F_STATE_OUT);
+    uint32_t t0;
+    int cnt;
+    tile_range(total_tiles, t0, cnt);
+    if (cnt <= 0) return;
+    const uint32_t sa = t0 >> tshift;
+    PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
+    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    ring_init(sm);
+    __syncthreads();
+    const uint32_t bar0 = su32(sm + kOffBar);
+    volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
+    volatile uint32_t* sxb = reinterpret_cast<volatile uint32_t*>(sm + kOffTag + 16);  // per stage
+    const int nr = (hp.kind[8] != 0) ? 3 : ((hp.kind[4] != 0) ? 2 : 1);  // rounds with ops
+    const uint32_t w = gt & 7u;
+    const uint32_t tx_issue = hx(hp, gt >> 3);             // gather bits 0-4 of issue units
+    const uint32_t tx_lev = hx(hp, gt & 255u);             // levels: column gb = gt (+256)
+
+    auto issue = [&](int k) {
+        if (k >= cnt) return;
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        bool any = false;
+        if (d.mix || fout) {
+            const uint32_t xb = deposit4(t & tmask, hp.freemask);
+            const uint32_t sb = su32(sm + s * kStageAmpBytes) + sw4(gt) * 16u;
+            const uint32_t x = (xb | w) ^ tx_issue;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)  // unit e = gt + 256 i: gb = gt>>3 | i<<5
+                cpa16(sb + i * (kGT * 16u), d.state + (x ^ hx(hp, static_cast<uint32_t>(i) << 5)));
+            if (fout && d.lev) {
+                const uint32_t lb = su32(sm + kOffLev + s * 8192u);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t col = gt + kGT * i;
+                    const uint32_t gx = (xb ^ tx_lev ^ (i ? hp.mask[8] : 0u)) & ~7u;
+                    cpa16(lb + col * 16u, d.lev + gx);
+                }
+            }
+            if (gt == 0) sxb[s] = xb;
+            any = true;
+        }
+        if (gt == 0) tag[s] = k;
+        if (any)
+            cpa_arrive(bar0 + s * 8u);
+        else
+            bar_arrive(bar0 + s * 8u);
+    };
+    if (g == 0) {
+        issue(0);
+        issue(2);
+    } else {
+        issue(1);
+    }
+
+    for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool mix = d.mix;
+        while (tag[s] != k) {
+        }
+        bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
+        if (!mix && !fout) {
+            issue(k + kStages);
+            continue;
+        }
+        const int nrr = mix ? nr : 1;  // no mixer: only f(z) to emit
+        const uint32_t xb = sxb[s] | w;
+        const double c = d.c, sn = d.s;
+        double2* st = reinterpret_cast<double2*>(sm + s * kStageAmpBytes);
+        const uint16_t* slev = reinterpret_cast<const uint16_t*>(sm + kOffLev + s * 8192u);
+        double2* const gstate = d.state;
+        double* const gf = d.fbuf;
+        const uint16_t* const glev = d.lev;
+        const double* const gval = d.val;
+        double2 a[16];
+        // tile index of amp j in round R
+        auto e_of = [&](auto R, int j) -> uint32_t {
+            if constexpr (decltype(R)::value == 0)
+                return w | (static_cast<uint32_t>(j) << 3) | ((gt >> 3) << 7);
+            else if constexpr (decltype(R)::value == 1)
+                return w | (((gt >> 3) & 15u) << 3) | (static_cast<uint32_t>(j) << 7) | ((gt >> 7) << 11);
+            else
+                return w | ((static_cast<uint32_t>(j >> 1) & 7u) << 3) | ((gt >> 3) << 6) |
+                       (static_cast<uint32_t>(j & 1) << 11);
+        };
+        // final round: write out (state and/or f) at xb ^ hx(gb)
+        auto emit = [&](auto R) {
+            constexpr int r = decltype(R)::value;
+            const uint32_t txt = r == 0 ? hx(hp, (gt >> 3) << 4)
+                               : r == 1 ? hx(hp, ((gt >> 3) & 15u) | ((gt >> 7) << 8))
+                                        : hx(hp, (gt >> 3) << 3);
+            const uint32_t xt = xb ^ txt;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t gidx = xt ^ hx(hp, gb_local<r>(j));
+                if (sout) __stcs(gstate + gidx, a[j]);
+                if (fout) {
+                    double cst;
+                    if (glev)
+                        cst = static_cast<double>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
+                    else
+                        cst = gval ? gval[gidx] : 1.0;
+                    __stcs(gf + gidx, __dmul_rn(nrm(a[j]), cst));
+                }
+            }
+        };
+        auto finish = [&](auto R) {
+            grp_sync(g);
+            if (!fout) issue(k + kStages);  // f reads the stage's levels: refill after
+            emit(R);
+            if (fout) {
+                grp_sync(g);
+                issue(k + kStages);
+            }
+        };
+        using R0 = std::integral_constant<int, 0>;
+        using R1 = std::integral_constant<int, 1>;
+        using R2 = std::integral_constant<int, 2>;
+        // round 0: gather bits 0-3 local
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R0{}, j))];
+        if (mix) ops_local<0, 4>(a, hp, c, sn);
+        if (nrr == 1) {
+            finish(R0{});
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) st[sw4(e_of(R0{}, j))] = a[j];
+        grp_sync(g);
+        // round 1: gather bits 4-7 local
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R1{}, j))];
+        ops_local<4, 4>(a, hp, c, sn);
+        if (nrr == 2) {
+            finish(R1{});
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) st[sw4(e_of(R1{}, j))] = a[j];
+        grp_sync(g);
+        // round 2: gather bit 8 local (j bit 0); j bits 1-3 carry gather bits 0-2
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R2{}, j))];
+        ops_local<8, 1>(a, hp, c, sn);
+        finish(R2{});
+    }
+}
+
+}  // namespace v4
+
+size_t pass4_smem() { return v4::kSmem; }
+
+namespace {
+int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QC_CUDA(cudaGetDevice(&dev));
+        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kSmem)));
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kSmem)));
+    }
+    return sms;
+}
+// Slots per launch such that every CTA's contiguous tile range spans <= kDescCap slots
+// (a CTA spans at most slots/grid + 3).
+int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
+}  // namespace
+
+int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
+                   int n_slots, cudaStream_t stream) {
+    const int sms = sm_count();
+    int launches = 0;
+    for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
+        const int n = std::min(n_slots - s0, slots_per_launch(sms));
+        const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
+        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+        v4::k_pass_a<<<grid, v4::kThreads, v4::kSmem, stream>>>(d_slots + s0, d_lp, layer, Q, flags,
+                                                               tiles);
+        QC_CUDA(cudaGetLastError());
+        ++launches;
+    }
+    return launches;
+}
+
+int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
+                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream) {
+    const int sms = sm_count();
+    int launches = 0;
+    for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
+        const int n = std::min(n_slots - s0, slots_per_launch(sms));
+        const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
+        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+        v4::k_pass_b<<<grid, v4::kThreads, v4::kSmem, stream>>>(d_slots + s0, d_lp, layer, Q, hp,
+                                                               flags, tiles);
+        QC_CUDA(cudaGetLastError());
+        ++launches;
+    }
+    return launches;
+}
+
+}  // namespace qcg

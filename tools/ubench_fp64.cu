@@ -38,6 +38,33 @@ __global__ void tput_dadd(double* out, int n, double x) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void tput_dmul(double* out, int n, double x) {
+    double a[8] = {1, 1, 2, 3, 4, 5, 6, 7};
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) a[k] = __dmul_rn(a[k], x);
+    double s = 0;
+    for (int k = 0; k < 8; ++k) s += a[k];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// the mixer_pair pattern: 8 DMUL + 4 DADD per pair, 4 independent pairs per thread
+__global__ void tput_rx(double* out, int n, double c, double s) {
+    double2 a[8];
+    for (int k = 0; k < 8; ++k) a[k] = make_double2(k * 0.1, 1.0 - k * 0.1);
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const double2 t0 = a[k], t1 = a[k + 1];
+            a[k].x = __dadd_rn(__dmul_rn(c, t0.x), __dmul_rn(s, t1.y));
+            a[k].y = __dsub_rn(__dmul_rn(c, t0.y), __dmul_rn(s, t1.x));
+            a[k + 1].x = __dadd_rn(__dmul_rn(s, t0.y), __dmul_rn(c, t1.x));
+            a[k + 1].y = __dsub_rn(__dmul_rn(c, t1.y), __dmul_rn(s, t0.x));
+        }
+    double r = 0;
+    for (int k = 0; k < 8; ++k) r += a[k].x + a[k].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
 int main() {
     double* d;
     float* f;
@@ -75,5 +102,24 @@ int main() {
     const double ops = double(sms) * 8 * 256 * it * 8;
     printf("DADD throughput: %.2f Tops/s (%d SMs, clock %d MHz) = %.1f per SM per cycle at max clock\n",
            ops / ms / 1e9, sms, clk / 1000, ops / (ms * 1e-3) / sms / (clk * 1e3));
+    tput_dmul<<<sms * 8, 256>>>(d, it, 1.0000001);
+    cudaEventRecord(e0);
+    tput_dmul<<<sms * 8, 256>>>(d, it, 1.0000001);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("DMUL throughput: %.2f Tops/s = %.1f per SM per cycle at max clock\n", ops / ms / 1e9,
+           ops / (ms * 1e-3) / sms / (clk * 1e3));
+    const int itr = 1024;
+    tput_rx<<<sms * 8, 256>>>(d, itr, 0.6, 0.8);
+    cudaEventRecord(e0);
+    tput_rx<<<sms * 8, 256>>>(d, itr, 0.6, 0.8);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops_rx = double(sms) * 8 * 256 * itr * 4 * 12;
+    printf("mixer_pair pattern (8 DMUL + 4 DADD): %.2f Tops/s = %.1f ops per SM per cycle; "
+           "%.3g amp-targets/s\n", ops_rx / ms / 1e9, ops_rx / (ms * 1e-3) / sms / (clk * 1e3),
+           ops_rx / 6 / (ms * 1e-3));
     return 0;
 }
