@@ -306,9 +306,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         double2* __restrict__ dst = d.state + base;
         grp_sync(g);  // the whole group is done with this stage: refill it
         issue(k + kStages);
-        if (mix) rx_local<0, 4>(a, c, sn);
+        // last target (bit 11 = local bit 3) pair by pair, each pair stored as soon as it
+        // is final: spreads the 64 KB of stores over the round instead of one burst
+        if (mix) rx_local<0, 3>(a, c, sn);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) __stcs(dst + ((j << 8) | gt), a[j]);
+        for (int j = 0; j < 8; ++j) {
+            if (mix) rx(a[j], a[j + 8], c, sn);
+            dst[(j << 8) | gt] = a[j];
+            dst[((j + 8) << 8) | gt] = a[j + 8];
+        }
     }
 }
 
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         cst = static_cast<double>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
                     else
                         cst = gval ? gval[gidx] : 1.0;
-                    __stcs(gf + gidx, __dmul_rn(nrm(a[j]), cst));
+                    gf[gidx] = __dmul_rn(nrm(a[j]), cst);  // stays in L2 for k_blocksum
                 }
             }
         };

@@ -65,6 +65,30 @@ __global__ void tput_rx(double* out, int n, double c, double s) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = r;
 }
 
+// pass-A-like register round: 16 amps/thread, RX on 4 local bits (ascending)
+__global__ void __launch_bounds__(512, 1) tput_rx16(double* out, int n, double c, double s) {
+    double2 a[16];
+    for (int k = 0; k < 16; ++k) a[k] = make_double2(k * 0.1 + threadIdx.x, 1.0 - k * 0.1);
+    for (int i = 0; i < n; ++i) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (!(j & (1 << b))) {
+                    double2& x0 = a[j];
+                    double2& x1 = a[j | (1 << b)];
+                    const double2 t0 = x0, t1 = x1;
+                    x0.x = __dadd_rn(__dmul_rn(c, t0.x), __dmul_rn(s, t1.y));
+                    x0.y = __dsub_rn(__dmul_rn(c, t0.y), __dmul_rn(s, t1.x));
+                    x1.x = __dadd_rn(__dmul_rn(s, t0.y), __dmul_rn(c, t1.x));
+                    x1.y = __dsub_rn(__dmul_rn(c, t1.y), __dmul_rn(s, t0.x));
+                }
+    }
+    double r = 0;
+    for (int k = 0; k < 16; ++k) r += a[k].x + a[k].y;
+    out[blockIdx.x * blockDim.x + threadIdx.x] = r;
+}
+
 int main() {
     double* d;
     float* f;
@@ -121,5 +145,17 @@ int main() {
     printf("mixer_pair pattern (8 DMUL + 4 DADD): %.2f Tops/s = %.1f ops per SM per cycle; "
            "%.3g amp-targets/s\n", ops_rx / ms / 1e9, ops_rx / (ms * 1e-3) / sms / (clk * 1e3),
            ops_rx / 6 / (ms * 1e-3));
+    for (int thr : {128, 256, 512}) {
+        const int it16 = 256;
+        tput_rx16<<<sms, thr>>>(d, it16, 0.6, 0.8);
+        cudaEventRecord(e0);
+        tput_rx16<<<sms, thr>>>(d, it16, 0.6, 0.8);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double o = double(sms) * thr * it16 * 4 * 8 * 12;
+        printf("rx16 (16 amps/thread, 4 targets/round), %d threads/SM: %.2f Tops/s = %.1f ops/SM/clk\n",
+               thr, o / ms / 1e9, o / (ms * 1e-3) / sms / (clk * 1e3));
+    }
     return 0;
 }
