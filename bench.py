@@ -327,6 +327,7 @@ def main():
                "h2d_bytes_per_step": (h1 - h0) // args.steps,
                "d2h_bytes_per_step": (d1 - d0) // args.steps,
                "ms_per_step": sum(t_e2e) / args.steps * 1e3,
+               "step_ms": [round(t * 1e3, 2) for t in t_e2e],
                "stage_s": {"partition": rep_e2e.partition_s, "qaoa": rep_e2e.qaoa_s,
                            "merge": rep_e2e.merge_s}}
     if rank != 0:

@@ -12,7 +12,9 @@
 // large state) uses a global bitonic sort instead.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "qc_internal.hpp"
 
@@ -168,6 +170,145 @@ __global__ void k_emit(const Key* __restrict__ keys, int k, uint32_t* __restrict
     probs[t] = __longlong_as_double(static_cast<long long>(keys[t].p));
 }
 
+// ---------------------------------------------------------------------------
+// K <= 32 (every configuration of the paper: K in {1,2,4,8}): one pass over the classes,
+// each thread keeping its best KT keys in registers (KT = K rounded up to a power of
+// two), then KT rounds of block-wide argmax; stage 2 merges the CTAs' lists the same
+// way. Keys are unique (bits are distinct), so the selection is exactly the reference's
+// total order (qaoa.hpp:179-186).
+// ---------------------------------------------------------------------------
+constexpr int kSmallThreads = 256;
+
+__device__ __forceinline__ bool kgt(uint64_t ap, uint32_t an, uint64_t bp, uint32_t bn) {
+    return ap > bp || (ap == bp && an > bn);
+}
+
+template <int KT>
+struct TopList {
+    uint64_t p[KT];
+    uint32_t n[KT];
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) {
+            p[i] = 0;
+            n[i] = 0;
+        }
+    }
+    // insert (descending); keys with p == 0 && n == 0 are "empty"
+    __device__ __forceinline__ void push(uint64_t xp, uint32_t xn) {
+#pragma unroll
+        for (int i = 0; i < KT; ++i) {
+            const bool gt = kgt(xp, xn, p[i], n[i]);
+            const uint64_t tp = p[i];
+            const uint32_t tn = n[i];
+            p[i] = gt ? xp : tp;
+            n[i] = gt ? xn : tn;
+            xp = gt ? tp : xp;
+            xn = gt ? tn : xn;
+        }
+    }
+    __device__ __forceinline__ void pop() {
+#pragma unroll
+        for (int i = 0; i + 1 < KT; ++i) {
+            p[i] = p[i + 1];
+            n[i] = n[i + 1];
+        }
+        p[KT - 1] = 0;
+        n[KT - 1] = 0;
+    }
+};
+
+// KT rounds of block argmax over the threads' list heads -> out[0..k)
+template <int KT>
+__device__ __forceinline__ void block_select(TopList<KT>& L, int k, Key* __restrict__ out) {
+    __shared__ uint64_t wp[kSmallThreads / 32];
+    __shared__ uint32_t wn[kSmallThreads / 32];
+    __shared__ uint32_t wt[kSmallThreads / 32];
+    __shared__ uint32_t win;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int r = 0; r < k; ++r) {
+        uint64_t bp = L.p[0];
+        uint32_t bn = L.n[0];
+        uint32_t bt = threadIdx.x;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t op = __shfl_xor_sync(0xffffffffu, bp, o);
+            const uint32_t on = __shfl_xor_sync(0xffffffffu, bn, o);
+            const uint32_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+            if (kgt(op, on, bp, bn)) {
+                bp = op;
+                bn = on;
+                bt = ot;
+            }
+        }
+        if (lane == 0) {
+            wp[warp] = bp;
+            wn[warp] = bn;
+            wt[warp] = bt;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int b = 0;
+            for (int w = 1; w < kSmallThreads / 32; ++w)
+                if (kgt(wp[w], wn[w], wp[b], wn[b])) b = w;
+            Key key;
+            key.p = wp[b];
+            key.nl = wn[b];
+            key.pad = 0;
+            out[r] = key;
+            win = wt[b];
+        }
+        __syncthreads();
+        if (threadIdx.x == win) L.pop();
+    }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kSmallThreads) k_topk_small_state(const double2* __restrict__ st,
+                                                                  int q, int sym, int fold,
+                                                                  uint64_t classes, int k,
+                                                                  Key* __restrict__ out) {
+    TopList<KT> L;
+    L.clear();
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kSmallThreads;
+    for (uint64_t c = static_cast<uint64_t>(blockIdx.x) * kSmallThreads + threadIdx.x; c < classes;
+         c += stride) {
+        const Key x = class_key(st, c, q, sym != 0, fold != 0);
+        L.push(x.p, x.nl);
+    }
+    block_select<KT>(L, k, out + static_cast<size_t>(blockIdx.x) * k);
+}
+
+template <int KT>
+__global__ void __launch_bounds__(kSmallThreads) k_topk_small_keys(const Key* __restrict__ in,
+                                                                 uint64_t count, int k,
+                                                                 Key* __restrict__ out) {
+    TopList<KT> L;
+    L.clear();
+    for (uint64_t c = threadIdx.x; c < count; c += kSmallThreads) L.push(in[c].p, in[c].nl);
+    block_select<KT>(L, k, out);
+}
+
+template <int KT>
+int launch_small(const double2* d_state, int q, bool sym, bool fold, uint64_t classes, int k,
+                 Key* keys, cudaStream_t stream) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        QC_CUDA(cudaGetDevice(&dev));
+        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const uint64_t want = (classes + 8 * kSmallThreads - 1) / (8 * kSmallThreads);  // >= 8 per thread
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 2u * sms)));
+    Key* part = keys + 1024;  // stage-1 lists (grid * k keys), final list at keys[0..k)
+    k_topk_small_state<KT><<<grid, kSmallThreads, 0, stream>>>(d_state, q, sym, fold, classes, k,
+                                                              grid == 1 ? keys : part);
+    if (grid > 1)
+        k_topk_small_keys<KT><<<1, kSmallThreads, 0, stream>>>(part, static_cast<uint64_t>(grid) * k,
+                                                              k, keys);
+    return grid > 1 ? 2 : 1;
+}
+
 uint64_t class_count(int q, bool fold) {
     return fold ? (uint64_t{1} << (q - 1)) : (uint64_t{1} << q);
 }
@@ -182,6 +323,7 @@ uint64_t pow2_ceil(uint64_t x) {
 
 size_t topk_scratch_bytes(int q, bool fold, int k) {
     const uint64_t classes = class_count(q, fold);
+    if (k <= 32) return (1024 + 2 * 148 * 32 + 64) * sizeof(Key) + 4096 * sizeof(Key);
     if (k > kChunk / 2) return pow2_ceil(classes) * sizeof(Key);
     const uint64_t chunks = (classes + kChunk - 1) / kChunk;
     return 2 * chunks * static_cast<uint64_t>(k) * sizeof(Key) + sizeof(Key);
@@ -201,6 +343,24 @@ int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void*
     } end_guard{prof, stream};
     Key* keys = static_cast<Key*>(d_scratch);
     int launches = 0;
+    if (k <= 32 && !std::getenv("QCG_TOPK_SORT")) {
+        const int kk = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(k), classes));
+        if (k <= 1)
+            launches = launch_small<1>(d_state, q, sym, fold, classes, kk, keys, stream);
+        else if (k <= 2)
+            launches = launch_small<2>(d_state, q, sym, fold, classes, kk, keys, stream);
+        else if (k <= 4)
+            launches = launch_small<4>(d_state, q, sym, fold, classes, kk, keys, stream);
+        else if (k <= 8)
+            launches = launch_small<8>(d_state, q, sym, fold, classes, kk, keys, stream);
+        else if (k <= 16)
+            launches = launch_small<16>(d_state, q, sym, fold, classes, kk, keys, stream);
+        else
+            launches = launch_small<32>(d_state, q, sym, fold, classes, kk, keys, stream);
+        k_emit<<<1, 32, 0, stream>>>(keys, k, d_bits, d_probs);
+        QC_CUDA(cudaGetLastError());
+        return launches + 1;
+    }
     if (k > kChunk / 2) {
         const uint64_t n = pow2_ceil(classes);
         k_fill_keys<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
