@@ -172,9 +172,14 @@ size_t qc_engine::max_slots(int Q, bool onchip) const {
     const size_t per = N * 16 + (onchip ? 0 : N * 8 + (N / 4096 + 2) * 16) + 64;
     size_t budget = mem_budget;
     if (budget == 0) {
-        size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = size_t{8} << 30;
-        budget = static_cast<size_t>(static_cast<double>(fr + states.cap + fbuf.cap) * 0.6);
+        // queried once: cudaMemGetInfo can stall for tens of ms behind the driver's
+        // deferred frees, and it sits on the per-step path
+        if (auto_budget == 0) {
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) fr = size_t{8} << 30;
+            auto_budget = static_cast<size_t>(static_cast<double>(fr + states.cap + fbuf.cap) * 0.6);
+        }
+        budget = auto_budget;
     }
     size_t s = budget / per;
     if (s < 1) s = 1;

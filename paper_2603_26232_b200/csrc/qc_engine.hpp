@@ -80,6 +80,7 @@ struct qc_engine {
     cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // extra streams: chunks overlap on the device
     uint64_t launches = 0;
     uint64_t mem_budget = 0;
+    mutable size_t auto_budget = 0;  // 60% of the free HBM seen at first use
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
     qcg::HostBuf hstage, hout;
     qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
