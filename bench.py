@@ -39,6 +39,9 @@ sys.path.insert(0, ROOT)
 
 PROFILE_STRIDE = 16  # per-kernel CUDA events on one launch in 16 (sampled, live)
 METRIC = "end-to-end Max-Cut solve time & subgraph-QAOA evals/s at 1/2/4/8 B200"
+# FP64 ceiling for the no-FMA butterfly stream, measured on B200 with tools/ubench_fp64.cu
+# (8 DMUL + 4 DADD per pair, all SMs): profiles/r1_ubench_fp64.txt
+FP64_PEAK_TOPS = 18.44
 UNIT = "evals/s"
 
 WORKLOADS = {
@@ -367,6 +370,8 @@ def main():
             traffic = tr.get("dram_bytes_per_launch") if tr else None
     except Exception:
         pass
+    fp64_peak = FP64_PEAK_TOPS
+    fp64_ach = d.get("fp64_ops", 0.0) / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind ==
@@ -376,8 +381,17 @@ def main():
                 "measured": "every launch of one single-stream step, CUDA events on its stream",
                 "launches": d["launches"],
                 "share_of_step": d["ms"] / iso_ms if iso_ms else None,
+                # the fp64 parity path forbids FMA: every butterfly is 8 DMUL + 4 DADD, so
+                # the FP64 pipe is the second ceiling (co-bound for the 12-target pass A)
+                "fp64": {"achieved_tops": fp64_ach, "peak_tops": fp64_peak,
+                         "frac": fp64_ach / fp64_peak,
+                         "ops_per_launch": d.get("fp64_ops", 0.0) / max(d["launches"], 1),
+                         "peak_source": "measured: tools/ubench_fp64.cu mixer_pair pattern "
+                                        "(profiles/r1_ubench_fp64.txt)"},
                 "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                 "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
+                                if v["ms"] > 0 else 0.0,
+                                "fp64_Tops": round(v.get("fp64_ops", 0.0) / (v["ms"] / 1e3) / 1e12, 2)
                                 if v["ms"] > 0 else 0.0}
                             for k, v in profile_iso.items() if v["launches"]},
                 # all engine kernels' algorithmic bytes of one step / timed step time

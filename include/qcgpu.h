@@ -175,6 +175,9 @@ int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
 int qc_engine_profile(qc_engine* e, int on);
 int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
                            double* bytes);
+/* Algorithmic FP64 operations (explicitly rounded DMUL/DADD; the path uses no FMA) of the
+ * profiled launches of a kernel kind, same window as qc_engine_profile_read. */
+int qc_engine_profile_read_fp64(qc_engine* e, int kind, double* fp64_ops);
 /* Host time of the lockstep optimiser: waiting for chunk results vs preparing the next
  * step (NM tell/ask, phase LUTs, staging, launches), and chunk-steps serviced. */
 int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t* steps,

@@ -353,8 +353,11 @@ class Engine:
             n = C.c_uint64(0)
             ms = C.c_double(0)
             b = C.c_double(0)
+            f = C.c_double(0)
             self._call("qc_engine_profile_read", C.c_int(k), C.byref(n), C.byref(ms), C.byref(b))
-            out[name] = dict(launches=int(n.value), ms=ms.value, bytes=b.value)  # sampled
+            self._call("qc_engine_profile_read_fp64", C.c_int(k), C.byref(f))
+            out[name] = dict(launches=int(n.value), ms=ms.value, bytes=b.value,
+                             fp64_ops=f.value)  # sampled
         return out
 
     def host_stats(self, reset: bool = False):

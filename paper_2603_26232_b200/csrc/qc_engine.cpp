@@ -686,6 +686,15 @@ int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* m
     });
 }
 
+int qc_engine_profile_read_fp64(qc_engine* e, int kind, double* fp64_ops) {
+    return guarded([&] {
+        check_engine(e);
+        if (kind < 0 || kind >= K_COUNT) config_error("unknown kernel kind");
+        e->prof.resolve();
+        if (fp64_ops) *fp64_ops = e->prof.ops[kind];
+    });
+}
+
 int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t* steps,
                          int reset) {
     return guarded([&] {

@@ -96,12 +96,13 @@ struct Prof {
     struct Rec {
         int kind;
         cudaEvent_t a, b;
-        double bytes;
+        double bytes, ops;
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     double ms[K_COUNT] = {};
     double bytes[K_COUNT] = {};
+    double ops[K_COUNT] = {};  // algorithmic FP64 operations (DMUL/DADD, no FMA)
     uint64_t count[K_COUNT] = {};
     cudaEvent_t ev() {
         if (!pool.empty()) {
@@ -113,11 +114,11 @@ struct Prof {
         cudaEventCreate(&e);
         return e;
     }
-    void begin(int kind, double b, cudaStream_t s) {
+    void begin(int kind, double b, cudaStream_t s, double fp64_ops = 0.0) {
         open_ = false;
         if (!on) return;
         if ((seen[kind]++ % static_cast<uint64_t>(stride)) != 0) return;
-        Rec r{kind, ev(), ev(), b};
+        Rec r{kind, ev(), ev(), b, fp64_ops};
         cudaEventRecord(r.a, s);
         recs.push_back(r);
         open_ = true;
@@ -135,6 +136,7 @@ struct Prof {
             cudaEventElapsedTime(&t, r.a, r.b);
             ms[r.kind] += t;
             bytes[r.kind] += r.bytes;
+            ops[r.kind] += r.ops;
             count[r.kind] += 1;
             pool.push_back(r.a);
             pool.push_back(r.b);
@@ -143,7 +145,7 @@ struct Prof {
     }
     void reset() {
         resolve();
-        for (int k = 0; k < K_COUNT; ++k) ms[k] = bytes[k] = 0, count[k] = 0, seen[k] = 0;
+        for (int k = 0; k < K_COUNT; ++k) ms[k] = bytes[k] = ops[k] = 0, count[k] = 0, seen[k] = 0;
     }
     ~Prof() {
         for (auto& r : recs) {

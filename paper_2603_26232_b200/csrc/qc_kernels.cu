@@ -712,7 +712,9 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         // pass A moves a slot if it initialises, phases or mixes it; levels read when phased
         const int active = fa ? n_slots : std::max(nph, nmix);
         const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
-        if (prof) prof->begin(K_PASS_LOW, ba, stream);
+        // FP64: 6 per amplitude for the phase, 6 per amplitude per RX target (12 targets)
+        const double oa = (nph * 6.0 + nmix * 72.0) * N;
+        if (prof) prof->begin(K_PASS_LOW, ba, stream, oa);
         if (v3)
             k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         else
@@ -729,7 +731,11 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                 bh = n_slots * N * (16.0 + 8.0 + 2.0 + ((fh & F_STATE_OUT) ? 16.0 : 0.0));
             else
                 bh = nmix * 32.0 * N;
-            if (prof) prof->begin(K_PASS_HIGH, bh, stream);
+            int items = 0;
+            for (int b = 0; b < kHighBits; ++b) items += plan.high[h].kind[b] != 0 ? 1 : 0;
+            // 6 per amplitude per pair op (RX target or mirror), + |a|^2 C(z) (4) when f is emitted
+            const double oh = nmix * 6.0 * items * N + ((fh & F_EXPECT) ? n_slots * 4.0 * N : 0.0);
+            if (prof) prof->begin(K_PASS_HIGH, bh, stream, oh);
             if (v3)
                 k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
                     d_slots, d_lp, l, Q, plan.high[h], fh);
@@ -751,7 +757,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             sum_attr = true;
         }
         const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl);
-        if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream);
+        if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
         k_blocksum<<<warps, 32, kSumSmem, stream>>>(tmap, n_slots, Q, plan.sym ? 1 : 0, d_partials,
                                                    d_tickets, d_out);
         if (prof) prof->end(stream);
