@@ -200,11 +200,11 @@ size_t qc_engine::chunk_slots(int Q, bool onchip, size_t n) const {
         if (v > 0) return std::min<size_t>(n, static_cast<size_t>(v));
     }
     // Chunks on separate streams: while one chunk's NM step is prepared on the host the
-    // other chunks' kernels run, and their grids fill each other's tails; one chunk's
-    // latency-bound expectation chains overlap another's passes. (Single-stream
-    // L2-sized chunks of 4-11 slots measured slower on B200: 134-241 ms vs 122 ms per C2
-    // solve in one chunk; two chunks on two streams: 108.5 ms.)
-    size_t chunks = 3;
+    // other chunk's kernels run. With the persistent v4 pass kernels (one CTA per SM) two
+    // chunks measured best on B200 for C2: 75.9 ms per solve vs 84.4 (1), 81.1 (3),
+    // 82.5 (4), 82.5 (6) -- every extra chunk adds per-launch prologue/tail and a
+    // latency-bound block-sum launch per lockstep step.
+    size_t chunks = 2;
     if (const char* env = std::getenv("QCG_CHUNKS")) chunks = std::max(1L, std::strtol(env, nullptr, 10));
     chunks = std::min(chunks, n);
     return std::max<size_t>(1, (n + chunks - 1) / chunks);
