@@ -74,8 +74,16 @@ HostGraph load_graph(const qc_graph* g) {
     h.u.reserve(static_cast<size_t>(g->m));
     h.v.reserve(static_cast<size_t>(g->m));
     h.w.reserve(static_cast<size_t>(g->m));
+    // duplicate detection (graph.hpp:37-50 add_edge rejects repeats): a bit per ordered
+    // pair u < v when that fits in 64 MB (n <= ~32k: every BASELINE config), else a hash set
+    const uint64_t nn = static_cast<uint64_t>(g->n);
+    const bool use_bits = nn * nn / 2 <= (uint64_t{64} << 23);
+    std::vector<uint64_t> bits;
     std::unordered_set<uint64_t> keys;
-    keys.reserve(static_cast<size_t>(g->m) * 2);
+    if (use_bits)
+        bits.assign(static_cast<size_t>((nn * nn / 2 + nn) / 64 + 1), 0);
+    else
+        keys.reserve(static_cast<size_t>(g->m) * 2);
     for (int i = 0; i < g->m; ++i) {
         uint32_t u = g->edges[i].u, v = g->edges[i].v;
         const double w = g->edges[i].w;
@@ -85,9 +93,15 @@ HostGraph load_graph(const qc_graph* g) {
         if (u == v) config_error("self-loop rejected at vertex " + std::to_string(u));
         if (w < 0.0 || std::isnan(w)) config_error("negative or NaN edge weight rejected");
         if (u > v) std::swap(u, v);
-        const uint64_t key = static_cast<uint64_t>(u) * static_cast<uint64_t>(g->n) + v;
-        if (!keys.insert(key).second)
-            config_error("duplicate edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
+        bool dup;
+        if (use_bits) {  // row-major upper triangle: u*(2n-u-1)/2 + (v-u-1)
+            const uint64_t k = static_cast<uint64_t>(u) * (2 * nn - u - 1) / 2 + (v - u - 1);
+            dup = (bits[k >> 6] >> (k & 63)) & 1u;
+            bits[k >> 6] |= uint64_t{1} << (k & 63);
+        } else {
+            dup = !keys.insert(static_cast<uint64_t>(u) * nn + v).second;
+        }
+        if (dup) config_error("duplicate edge (" + std::to_string(u) + "," + std::to_string(v) + ")");
         h.u.push_back(u);
         h.v.push_back(v);
         h.w.push_back(w);

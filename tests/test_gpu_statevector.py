@@ -128,3 +128,14 @@ def test_errors_map_to_reference_types(engine):
         engine.solve_subgraph(21, [(0, 20)])  # default cap 20 (test_qaoa.cpp:243-254)
     with pytest.raises(ConfigError):
         engine.run_ansatz(3, [(0, 0)], [0.1], [0.1])  # self-loop
+
+
+@pytest.mark.parametrize("n", [3, 40000])  # bitset path (n <= ~32k) and hash-set path
+def test_duplicate_edges_rejected_like_add_edge(engine, n):
+    """graph.hpp:37-50: a repeated pair (either orientation) is a config_error."""
+    from paper_2603_26232_b200 import ConfigError
+    with pytest.raises(ConfigError):
+        engine.cost_table(n, [(0, 1, 1.0), (1, 2, 1.0), (1, 0, 1.0)])
+    if n == 3:
+        out, integral, mx = engine.cost_table(n, [(0, 1, 1.0), (1, 2, 1.0), (0, 2, 1.0)])
+        assert integral and mx == 2.0
