@@ -108,6 +108,7 @@ HostGraph load_graph(const qc_graph* g) {
         h.total += w;
         if (w != std::floor(w) || w < 0.0) h.integral = false;
     }
+    h.all_int = h.integral && h.total <= 4.0e18;
     if (h.total > 65535.0) h.integral = false;
     return h;
 }

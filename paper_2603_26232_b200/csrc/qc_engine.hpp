@@ -22,6 +22,7 @@ struct HostGraph {
     std::vector<double> w;
     bool integral = true;
     double total = 0.0;
+    bool all_int = true;  // every weight a nonnegative integer, total <= 4e18 (merge scoring)
 };
 HostGraph load_graph(const qc_graph* g);
 

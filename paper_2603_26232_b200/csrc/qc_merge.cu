@@ -24,6 +24,10 @@
 // device-resident assignment; the next window's seam bit is read on the device.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstdint>
 #include <array>
@@ -405,6 +409,75 @@ __global__ void k_cut_int(const uint32_t* __restrict__ eu, const uint32_t* __res
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+// ---------------------------------------------------------------------------
+// Device-side edge classification for the integral windowed/level merge (replaces host
+// bucketing of every edge: merge.hpp:103-113 level_edge_buckets, grouped for the unary /
+// pair tables). Bins: fixed edges of level hi (lo in an earlier window) -> bin hi;
+// in-window edges (hi, lo) -> bin M + hi*kMaxL + (lo - win_start[hi]). Sums over a bin are
+// integers, so the scatter order is immaterial.
+// ---------------------------------------------------------------------------
+struct ClassArgs {
+    const uint32_t* eu;
+    const uint32_t* ev;
+    const double* ew;
+    long long m;
+    const int32_t* fl;        // first level of each vertex
+    const int32_t* ws;        // window start of each level
+    const int32_t* first;     // first global vertex of each level
+    int M;
+};
+
+__device__ __forceinline__ void classify(const ClassArgs& A, long long k, int& bin, int32_t& khi,
+                                         int32_t& kx, int64_t& w) {
+    uint32_t a = A.eu[k], b = A.ev[k];
+    int la = A.fl[a], lb = A.fl[b];
+    if (la > lb) {
+        const int t = la;
+        la = lb;
+        lb = t;
+        const uint32_t tv = a;
+        a = b;
+        b = tv;
+    }
+    // b: vertex on the higher level lb, a: on the lower level la
+    w = static_cast<int64_t>(A.ew[k]);
+    khi = static_cast<int32_t>(b) - A.first[lb];
+    if (la < A.ws[lb]) {
+        bin = lb;
+        kx = static_cast<int32_t>(a);  // global id of the fixed endpoint
+    } else {
+        bin = A.M + lb * kMaxL + (la - A.ws[lb]);
+        kx = static_cast<int32_t>(a) - A.first[la];
+    }
+}
+
+__global__ void k_edge_hist(ClassArgs A, unsigned* __restrict__ hist) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < A.m;
+         k += (long long)gridDim.x * blockDim.x) {
+        int bin;
+        int32_t khi, kx;
+        int64_t w;
+        classify(A, k, bin, khi, kx, w);
+        atomicAdd(hist + bin, 1u);
+    }
+}
+
+__global__ void k_edge_scatter(ClassArgs A, unsigned* __restrict__ cursor,
+                               FixedEdge* __restrict__ fixed, PairEdge* __restrict__ pairs) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < A.m;
+         k += (long long)gridDim.x * blockDim.x) {
+        int bin;
+        int32_t khi, kx;
+        int64_t w;
+        classify(A, k, bin, khi, kx, w);
+        const unsigned pos = atomicAdd(cursor + bin, 1u);
+        if (bin < A.M)
+            fixed[pos] = FixedEdge{khi, kx, w};
+        else
+            pairs[pos] = PairEdge{khi, kx, w};
+    }
+}
+
 thread_local DeviceArena* g_arena = nullptr;
 
 template <typename T>
@@ -469,9 +542,23 @@ double estimate_paths(const int32_t* counts, int M, bool halve) {
     return est;
 }
 
+namespace {
+struct MTrace {
+    bool on = std::getenv("QCG_TRACE_MERGE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "merge %-12s %8.2f ms\n", what, std::chrono::duration<double>(now - t).count() * 1e3);
+        t = now;
+    }
+};
+}  // namespace
+
 MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, bool full_graph,
                       cudaStream_t st, uint64_t* launches, Prof* prof, uint64_t* h2d, uint64_t* d2h,
                       DeviceArena* arena) {
+    MTrace tr;
     Prof dummy;
     if (!prof) prof = &dummy;
     uint64_t h2d_local = 0, d2h_local = 0;
@@ -494,20 +581,27 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     auto S = [](int i) { return static_cast<size_t>(i); };
 
     // ---- first level of every vertex (merge.hpp:106-108), integrality
+    // edges arrive either as the pipeline's SoA arrays or as qc_edge AoS (C-ABI merges)
+    auto EU = [&](long long k) { return in.eu ? in.eu[k] : in.edges[k].u; };
+    auto EV = [&](long long k) { return in.eu ? in.ev[k] : in.edges[k].v; };
+    auto EW = [&](long long k) { return in.eu ? in.ew[k] : in.edges[k].w; };
     std::vector<int32_t> fl(S(n), 0);
     for (int i = M - 1; i >= 0; --i)
         for (int v = in.first[i]; v <= in.last[i]; ++v) fl[S(v)] = i;
-    bool integral = true;
-    long double total = 0;
-    for (long long k = 0; k < in.m; ++k) {
-        const double w = in.edges[k].w;
-        if (!(w >= 0) || w != static_cast<double>(static_cast<int64_t>(w))) integral = false;
-        total += w;
+    bool integral = in.all_int != 0;
+    if (in.all_int < 0) {
+        long double total = 0;
+        for (long long k = 0; k < in.m; ++k) {
+            const double w = EW(k);
+            if (!(w >= 0) || w != static_cast<double>(static_cast<int64_t>(w))) integral = false;
+            total += w;
+        }
+        if (total > 4.0e18L) integral = false;
     }
-    if (total > 4.0e18L) integral = false;
     for (int i = 0; i < M; ++i)
         if (in.widths[i] > 32) internal_error("piece wider than 32 vertices in merge");
 
+    tr.mark("fl+integral");
     std::vector<int32_t> bits_off(S(M));
     for (int i = 0, off = 0; i < M; ++i) {
         bits_off[S(i)] = off;
@@ -569,79 +663,110 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         utab_size += in.counts[i];
     }
 
+    tr.mark("lists");
     // ---- scoring data
     std::vector<int32_t> pair_off;
-    std::vector<FixedEdge> fixed_edges;
     std::vector<XEdge> xedges, all_edges;
     int64_t* d_intra = nullptr;
     int64_t* d_ptab = nullptr;
     int64_t* d_utab = nullptr;
+    FixedEdge* d_fixed_edges = nullptr;
+    uint32_t* d_eu = nullptr;
+    uint32_t* d_ev = nullptr;
+    double* d_ew = nullptr;
     if (integral) {
-        // groups: (hi level, lo level in the same window); edges to earlier windows are
-        // "fixed" edges of their hi level, folded into the unary table per window.
-        std::vector<std::vector<int32_t>> gid(S(M));
-        for (int i = 0; i < M; ++i) gid[S(i)].assign(S(i - win_start[S(i)] + 1), -1);
-        std::vector<PairGroup> groups;
-        std::vector<std::vector<PairEdge>> pedges;
-        std::vector<std::vector<FixedEdge>> fixed_by_level(S(M));
-        auto group_of = [&](int hi, int lo) -> int32_t {
-            int32_t& g = gid[S(hi)][S(lo - win_start[S(hi)])];
-            if (g < 0) {
-                g = static_cast<int32_t>(groups.size());
-                groups.push_back({hi, lo, 0, 0, 0});
-                pedges.emplace_back();
-            }
-            return g;
-        };
-        for (int i = 0; i < M; ++i) group_of(i, i);  // every level has an intra table
-        for (long long k = 0; k < in.m; ++k) {
-            const qc_edge_t& e = in.edges[k];
-            int lo = fl[S(e.u)], hi = fl[S(e.v)];
-            uint32_t vh = e.v, vl = e.u;
-            if (lo > hi) {
-                std::swap(lo, hi);
-                std::swap(vh, vl);
-            }
-            const int64_t w = static_cast<int64_t>(e.w);
-            if (lo < win_start[S(hi)]) {
-                fixed_by_level[S(hi)].push_back(
-                    {static_cast<int32_t>(vh) - in.first[hi], static_cast<int32_t>(vl), w});
+        // Edges go to the device once (also used by the final re-score); the GPU bins them
+        // by (higher level, lower level in the same window) or as "fixed" edges of their
+        // higher level (lower endpoint in an earlier window: folded into the unary table
+        // per window). The host only scans the bin histogram.
+        const size_t m = static_cast<size_t>(in.m);
+        d_eu = dalloc<uint32_t>(keep, m);
+        d_ev = dalloc<uint32_t>(keep, m);
+        d_ew = dalloc<double>(keep, m);
+        if (m) {
+            if (in.eu) {
+                QC_CUDA(cudaMemcpyAsync(d_eu, in.eu, m * 4, cudaMemcpyHostToDevice, st));
+                QC_CUDA(cudaMemcpyAsync(d_ev, in.ev, m * 4, cudaMemcpyHostToDevice, st));
+                QC_CUDA(cudaMemcpyAsync(d_ew, in.ew, m * 8, cudaMemcpyHostToDevice, st));
             } else {
-                pedges[S(group_of(hi, lo))].push_back(
-                    {static_cast<int32_t>(vh) - in.first[hi], static_cast<int32_t>(vl) - in.first[lo], w});
+                std::vector<uint32_t> hu(m), hv(m);
+                std::vector<double> hw(m);
+                for (size_t k = 0; k < m; ++k) {
+                    hu[k] = in.edges[k].u;
+                    hv[k] = in.edges[k].v;
+                    hw[k] = in.edges[k].w;
+                }
+                QC_CUDA(cudaMemcpyAsync(d_eu, hu.data(), m * 4, cudaMemcpyHostToDevice, st));
+                QC_CUDA(cudaMemcpyAsync(d_ev, hv.data(), m * 4, cudaMemcpyHostToDevice, st));
+                QC_CUDA(cudaMemcpyAsync(d_ew, hw.data(), m * 8, cudaMemcpyHostToDevice, st));
+                QC_CUDA(cudaStreamSynchronize(st));  // host staging goes out of scope
             }
+            *h2d += m * 16;
         }
-        std::vector<PairEdge> flat;
-        std::vector<PairGroup> gi, gp;
-        int64_t ptab_size = 0;
-        for (size_t g = 0; g < groups.size(); ++g) {
-            PairGroup& G = groups[g];
-            G.e_off = static_cast<int32_t>(flat.size());
-            G.e_len = static_cast<int32_t>(pedges[g].size());
-            flat.insert(flat.end(), pedges[g].begin(), pedges[g].end());
-            if (G.hi == G.lo) {
-                G.out_off = wl[S(G.hi)].u_off;
-                gi.push_back(G);
-            } else {
-                G.out_off = static_cast<int32_t>(ptab_size);
-                ptab_size += static_cast<int64_t>(in.counts[G.hi]) * in.counts[G.lo];
-                gp.push_back(G);
-            }
+        std::vector<int32_t> first_l(in.first, in.first + M);
+        auto* d_fl = dupload(keep, fl, st);
+        auto* d_ws = dupload(keep, win_start, st);
+        auto* d_firstl = dupload(keep, first_l, st);
+        const size_t nbins = S(M) + S(M) * kMaxL;
+        auto* d_hist = dalloc<unsigned>(keep, nbins);
+        QC_CUDA(cudaMemsetAsync(d_hist, 0, nbins * 4, st));
+        ClassArgs CA{d_eu, d_ev, d_ew, in.m, d_fl, d_ws, d_firstl, M};
+        const unsigned cblocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((in.m + 255) / 256, 148 * 16)));
+        if (m) {
+            prof->begin(K_MERGE_OTHER, static_cast<double>(m) * 16.0, st);
+            k_edge_hist<<<cblocks, 256, 0, st>>>(CA, d_hist);
+            prof->end(st);
+            ++*launches;
         }
+        std::vector<unsigned> hist(nbins);
+        QC_CUDA(cudaMemcpyAsync(hist.data(), d_hist, nbins * 4, cudaMemcpyDeviceToHost, st));
+        QC_CUDA(cudaStreamSynchronize(st));
+        *d2h += nbins * 4;
+        // fixed edges: bins [0, M) in level order; pair edges: bins M + hi*kMaxL + (lo-ws)
+        std::vector<unsigned> cursor(nbins);
+        unsigned nfixed = 0, npair = 0;
         for (int i = 0; i < M; ++i) {
             WinLevel& L = wl[S(i)];
+            L.fixed_off = static_cast<int32_t>(nfixed);
+            L.fixed_len = static_cast<int32_t>(hist[S(i)]);
+            cursor[S(i)] = nfixed;
+            nfixed += hist[S(i)];
+        }
+        std::vector<PairGroup> gi, gp;
+        int64_t ptab_size = 0;
+        for (int i = 0; i < M; ++i) {
+            const int s0 = win_start[S(i)];
+            WinLevel& L = wl[S(i)];
             L.pair_base = static_cast<int32_t>(pair_off.size());
-            for (int j = win_start[S(i)]; j < i; ++j) {
-                const int32_t g = gid[S(i)][S(j - win_start[S(i)])];
-                pair_off.push_back(g < 0 ? -1 : groups[S(g)].out_off);
+            for (int j = s0; j <= i; ++j) {
+                const size_t bin = S(M) + S(i) * kMaxL + S(j - s0);
+                const unsigned len = hist[bin];
+                cursor[bin] = npair;
+                PairGroup G{i, j, 0, static_cast<int32_t>(npair), static_cast<int32_t>(len)};
+                npair += len;
+                if (j == i) {  // every level has an intra table
+                    G.out_off = L.u_off;
+                    gi.push_back(G);
+                } else if (len) {
+                    G.out_off = static_cast<int32_t>(ptab_size);
+                    ptab_size += static_cast<int64_t>(in.counts[i]) * in.counts[j];
+                    gp.push_back(G);
+                    pair_off.push_back(G.out_off);
+                } else {
+                    pair_off.push_back(-1);
+                }
             }
-            L.fixed_off = static_cast<int32_t>(fixed_edges.size());
-            L.fixed_len = static_cast<int32_t>(fixed_by_level[S(i)].size());
-            fixed_edges.insert(fixed_edges.end(), fixed_by_level[S(i)].begin(),
-                               fixed_by_level[S(i)].end());
+        }
+        auto* d_cursor = dupload(keep, cursor, st);
+        d_fixed_edges = dalloc<FixedEdge>(keep, nfixed);
+        auto* d_pe = dalloc<PairEdge>(keep, npair);
+        if (m) {
+            prof->begin(K_MERGE_OTHER, static_cast<double>(m) * 32.0, st);
+            k_edge_scatter<<<cblocks, 256, 0, st>>>(CA, d_cursor, d_fixed_edges, d_pe);
+            prof->end(st);
+            ++*launches;
         }
         std::vector<int32_t> counts_v(in.counts, in.counts + M);
-        auto* d_pe = dupload(keep, flat, st);
         auto* d_bits0 = dupload(keep, hbits, st);
         auto* d_boff = dupload(keep, bits_off, st);
         auto* d_counts = dupload(keep, counts_v, st);
@@ -650,7 +775,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         d_ptab = dalloc<int64_t>(keep, static_cast<size_t>(ptab_size));
         if (!gi.empty()) {
             auto* d_gi = dupload(keep, gi, st);
-            prof->begin(K_MERGE_TABLES, static_cast<double>(flat.size()) * 16.0, st);
+            prof->begin(K_MERGE_TABLES, static_cast<double>(npair) * 16.0, st);
             k_pair_tables<<<static_cast<unsigned>(gi.size()), 128, 0, st>>>(d_gi, d_pe, d_bits0, d_boff,
                                                                            d_counts, d_intra);
             prof->end(st);
@@ -668,10 +793,10 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     } else {
         std::vector<std::vector<XEdge>> buckets(S(M));
         for (long long k = 0; k < in.m; ++k) {
-            const qc_edge_t& e = in.edges[k];
-            XEdge x{e.u, e.v, e.w, fl[S(e.u)], fl[S(e.v)]};
+            const uint32_t eu = EU(k), ev = EV(k);
+            XEdge x{eu, ev, EW(k), fl[S(eu)], fl[S(ev)]};
             all_edges.push_back(x);
-            buckets[S(std::max(fl[S(e.u)], fl[S(e.v)]))].push_back(x);
+            buckets[S(std::max(fl[S(eu)], fl[S(ev)]))].push_back(x);
         }
         for (int i = 0; i < M; ++i) {
             wl[S(i)].bucket_off = static_cast<int32_t>(xedges.size());
@@ -680,13 +805,13 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         }
     }
 
+    tr.mark("tables");
     // ---- upload common data
     std::vector<int32_t> first_v(in.first, in.first + M);
     auto* d_wl = dupload(keep, wl, st);
     auto* d_lists = dupload(keep, lists, st);
     auto* d_bits = dupload(keep, hbits, st);
     auto* d_pair_off = dupload(keep, pair_off, st);
-    auto* d_fixed_edges = dupload(keep, fixed_edges, st);
     auto* d_xedges = dupload(keep, xedges, st);
     auto* d_all = dupload(keep, all_edges, st);
     auto* d_first = dupload(keep, first_v, st);
@@ -785,6 +910,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         QC_CUDA(cudaGetLastError());
     }
 
+    tr.mark("windows-enq");
     MergeOutput out;
     out.assignment.resize(S(n));
     int dead = 0;
@@ -793,17 +919,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     QC_CUDA(cudaMemcpyAsync(&dead, d_dead, sizeof(int), cudaMemcpyDeviceToHost, st));
     *d2h += S(n) + sizeof(uint64_t) + sizeof(int);
     if (integral && in.m > 0) {
-        // cut_value re-score on the device (exact for integral weights)
-        std::vector<uint32_t> eu(S(static_cast<int>(in.m))), ev(eu.size());
-        std::vector<double> ew(eu.size());
-        for (long long k = 0; k < in.m; ++k) {
-            eu[S(static_cast<int>(k))] = in.edges[k].u;
-            ev[S(static_cast<int>(k))] = in.edges[k].v;
-            ew[S(static_cast<int>(k))] = in.edges[k].w;
-        }
-        auto* d_eu = dupload(keep, eu, st);
-        auto* d_ev = dupload(keep, ev, st);
-        auto* d_ew = dupload(keep, ew, st);
+        // cut_value re-score on the device (exact for integral weights), edges resident
         auto* d_cut = dalloc<unsigned long long>(keep, 1);
         QC_CUDA(cudaMemsetAsync(d_cut, 0, sizeof(unsigned long long), st));
         const long long blocks = std::min<long long>((in.m + 255) / 256, 148 * 8);
@@ -820,9 +936,10 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         QC_CUDA(cudaStreamSynchronize(st));
         double v = 0.0;  // graph.hpp:126-134, edge-list order
         for (long long k = 0; k < in.m; ++k)
-            if (out.assignment[in.edges[k].u] != out.assignment[in.edges[k].v]) v += in.edges[k].w;
+            if (out.assignment[EU(k)] != out.assignment[EV(k)]) v += EW(k);
         out.value = v;
     }
+    tr.mark("rescore+sync");
     if (dead) config_error("no compatible candidate chain exists");
     return out;
 }

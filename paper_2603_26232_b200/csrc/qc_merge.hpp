@@ -18,7 +18,11 @@ struct qc_edge_t {  // == qc_edge (qcgpu.h) == qcut::Edge layout
 struct MergeInput {
     int n = 0;                       // vertices
     long long m = 0;                 // edges
-    const qc_edge_t* edges = nullptr;
+    const qc_edge_t* edges = nullptr;  // AoS edges, or null when the SoA arrays are given
+    const uint32_t* eu = nullptr;    // SoA edges (u < v) -- the pipeline's HostGraph arrays
+    const uint32_t* ev = nullptr;
+    const double* ew = nullptr;
+    int all_int = -1;                // every weight a nonnegative integer (-1: compute)
     int levels = 0;                  // pool levels
     const int32_t* widths = nullptr;
     const int32_t* counts = nullptr;

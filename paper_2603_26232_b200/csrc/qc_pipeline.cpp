@@ -4,6 +4,7 @@
 // points and the fixed-size solve records used by the multi-GPU gather.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <memory>
 #include <cmath>
 #include <cstring>
@@ -158,12 +159,14 @@ Pool build_pools(const std::vector<SolveOut>& sets) {
 
 MergeInput make_input(const HostGraph& g, std::vector<qc_edge_t>& store, const Pool& pool,
                       const std::vector<int32_t>& first, const std::vector<int32_t>& last) {
-    store.resize(g.u.size());
-    for (size_t k = 0; k < g.u.size(); ++k) store[k] = {g.u[k], g.v[k], g.w[k]};
+    (void)store;  // the merge reads the HostGraph's SoA edge arrays directly
     MergeInput in;
     in.n = g.n;
-    in.m = static_cast<long long>(store.size());
-    in.edges = store.data();
+    in.m = static_cast<long long>(g.u.size());
+    in.eu = g.u.data();
+    in.ev = g.v.data();
+    in.ew = g.w.data();
+    in.all_int = g.all_int ? 1 : 0;
     in.levels = static_cast<int>(pool.widths.size());
     in.widths = pool.widths.data();
     in.counts = pool.counts.data();
@@ -337,9 +340,13 @@ std::vector<SolveOut> solve_range(qc_engine* e, const Partition& P, const qc_run
 
 MergeOutput merge_stage(qc_engine* e, const HostGraph& g, const Partition& P,
                         const std::vector<SolveOut>& solves, const qc_run_config* c, bool* windowed) {
+    const auto tm0 = std::chrono::steady_clock::now();
     const Pool pool = build_pools(solves);
     std::vector<qc_edge_t> store;
     const MergeInput in = make_input(g, store, pool, P.first, P.last);
+    if (std::getenv("QCG_TRACE_MERGE"))
+        std::fprintf(stderr, "merge pools+input %8.2f ms\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - tm0).count() * 1e3);
     const int M = static_cast<int>(P.first.size());
     int mode = c->merge_mode;  // pipeline.hpp:307-311
     if (mode == 0)
