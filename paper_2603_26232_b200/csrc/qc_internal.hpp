@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace qcg {
@@ -171,11 +172,32 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                  unsigned* d_tickets, double* d_out, cudaStream_t stream,
                  const ChainStats* stats = nullptr, Prof* prof = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
-// v4 streaming passes (qc_pass.cu): persistent, one CTA per SM
+// v4 streaming passes (qc_pass.cu): persistent, one CTA per SM. pdl: launched with
+// programmatic stream serialization (the kernel's prologue overlaps the previous kernel's
+// tail; it waits with griddepcontrol.wait before touching state memory). Only for a
+// kernel whose stream predecessor is a kernel of the same chain.
 int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
-                   int n_slots, cudaStream_t stream);
+                   int n_slots, cudaStream_t stream, bool pdl = false);
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
-                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream);
+                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream,
+                   bool pdl = false);
+
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute
+template <typename... KArgs, typename... Args>
+void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+               bool pdl, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    QC_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,
 // ordered by (prob desc, lex asc) (qaoa.hpp:179-182). d_scratch sized by topk_scratch_bytes.

@@ -497,6 +497,7 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
         asm volatile("mbarrier.init.shared.b64 [%0], 1;\n" ::"r"(smem_u32(mbar + lane)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncwarp();
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");  // f is written by the previous pass
     auto issue = [&](int c) {
         if (c >= kChunks || lane != 0) return;
         const int st = c % kSumStages;
@@ -705,6 +706,11 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const char* e = std::getenv("QCG_PASS");
         return e && std::atoi(e) == 3;
     }();
+    // Programmatic dependent launch for every kernel whose stream predecessor is a kernel
+    // of this chain (the first one follows the staging copy). Off by default: with two
+    // chunk streams the early-scheduled dependent CTAs hold SMs the other stream's kernels
+    // need (C2: 82.8 ms/solve with PDL vs 75.6 without). QCG_PDL=1 enables it.
+    static const bool pdl_ok = std::getenv("QCG_PDL") != nullptr;
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
@@ -718,7 +724,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         if (v3)
             k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         else
-            launch_pass_a4(d_slots, d_lp, l, Q, fa, n_slots, stream);
+            launch_pass_a4(d_slots, d_lp, l, Q, fa, n_slots, stream, pdl_ok && l > 0);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -740,7 +746,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                 k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
                     d_slots, d_lp, l, Q, plan.high[h], fh);
             else
-                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh, n_slots, stream);
+                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh, n_slots, stream, pdl_ok);
             if (prof) prof->end(stream);
             ++launches;
         }
@@ -758,8 +764,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         }
         const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
-        k_blocksum<<<warps, 32, kSumSmem, stream>>>(tmap, n_slots, Q, plan.sym ? 1 : 0, d_partials,
-                                                   d_tickets, d_out);
+        launch_ex(k_blocksum, dim3(warps), dim3(32), kSumSmem, stream, pdl_ok, tmap, n_slots, Q,
+                  plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());

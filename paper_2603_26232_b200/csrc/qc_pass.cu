@@ -87,6 +87,12 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     }
 }
+// Programmatic dependent launch: let the next kernel of the chain be scheduled now (its
+// CTAs land as ours exit), and wait for the previous kernel's completion before any
+// state access (no-ops when the launch did not set the attribute).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 __device__ __forceinline__ void grp_sync(uint32_t g) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(g + 1u), "n"(kGT) : "memory");
 }
@@ -187,6 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
     ring_init(sm);
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();
     const uint32_t bar0 = su32(sm + kOffBar);
     volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
 
@@ -384,6 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
     ring_init(sm);
     __syncthreads();
+    pdl_trigger();
+    pdl_wait();
     const uint32_t bar0 = su32(sm + kOffBar);
     volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
     volatile uint32_t* sxb = reinterpret_cast<volatile uint32_t*>(sm + kOffTag + 16);  // per stage
@@ -549,15 +559,15 @@ int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
 }  // namespace
 
 int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
-                   int n_slots, cudaStream_t stream) {
+                   int n_slots, cudaStream_t stream, bool pdl) {
     const int sms = sm_count();
     int launches = 0;
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
         const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
-        v4::k_pass_a<<<grid, v4::kThreads, v4::kSmem, stream>>>(d_slots + s0, d_lp, layer, Q, flags,
-                                                               tiles);
+        launch_ex(v4::k_pass_a, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream, pdl || s0 > 0,
+                  d_slots + s0, d_lp, layer, Q, flags, tiles);
         QC_CUDA(cudaGetLastError());
         ++launches;
     }
@@ -565,7 +575,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
 }
 
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
-                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream) {
+                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream, bool pdl) {
     const int sms = sm_count();
     int launches = 0;
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
