@@ -78,7 +78,9 @@ def test_plus_state(engine, oracle):
 
 
 @pytest.mark.parametrize("q,k,fold", [(2, 2, True), (2, 4, False), (5, 16, True), (9, 4, True),
-                                      (12, 7, False), (14, 8, True), (16, 1500, True)])
+                                      (12, 7, False), (14, 8, True), (16, 1500, True),
+                                      # register top-K boundary (K <= 32) vs the sort paths
+                                      (11, 17, False), (18, 32, True), (18, 33, True)])
 def test_top_candidates_random(engine, oracle, q, k, fold):
     s = rand_state(q, q * 7 + k)
     b0, p0 = oracle.top_candidates(s, k, fold)
@@ -100,7 +102,7 @@ def test_top_candidates_plateaus(engine, oracle):
     # QAOA states of sparse graphs have huge plateaus of exactly equal probabilities
     e = oracle.generate_er(10, 0.1, 0)
     a, _ = oracle.run_ansatz(10, e, [1.1], [0.4])
-    for k in (1, 4, 37, 512):
+    for k in (1, 2, 4, 17, 32, 37, 512):
         b0, p0 = oracle.top_candidates(a, k, True)
         b1, p1 = engine.top_candidates(a, k, True)
         assert np.array_equal(b1, b0) and np.array_equal(p1, p0)
