@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
         if (!act) {
+            grp_sync(g);  // every thread has seen tag k before the refill overwrites it
             issue(k + kStages);
             continue;  // identity layer: memory already holds the result
         }
@@ -449,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
         if (!mix && !fout) {
+            grp_sync(g);  // every thread has seen tag k before the refill overwrites it
             issue(k + kStages);
             continue;
         }

@@ -145,3 +145,31 @@ def test_duplicate_edges_rejected_like_add_edge(engine, n):
     if n == 3:
         out, integral, mx = engine.cost_table(n, [(0, 1, 1.0), (1, 2, 1.0), (0, 2, 1.0)])
         assert integral and mx == 2.0
+
+
+@pytest.mark.parametrize("q,layers", [(10, 1), (14, 2), (20, 2)])
+def test_fractional_weights_within_tolerance(engine, oracle, q, layers):
+    """Non-integral weights take statevector.hpp:162-164 (per-amplitude std::polar). The
+    device evaluates sin/cos itself; glibc's sin/cos are not correctly rounded (~0.13% of
+    arguments differ from the correctly rounded value by 1 ulp), so this path is held to
+    the north-star fp64 tolerance (1e-10 relative), not to bit equality."""
+    rng = np.random.default_rng(q)
+    e = oracle.generate_er(q, 0.3, q).copy()
+    e["w"] = rng.uniform(0.1, 1.1, len(e))
+    g = rng.uniform(0.2, np.pi, layers)
+    b = rng.uniform(0.2, np.pi, layers)
+    a0, x0 = oracle.run_ansatz(q, e, g, b)
+    a1, x1 = engine.run_ansatz(q, e, g, b)
+    assert abs(x1 - x0) <= 1e-10 * abs(x0)
+    assert np.max(np.abs(a1 - a0)) <= 1e-10 * np.max(np.abs(a0))
+
+
+@pytest.mark.parametrize("q", [14, 20])
+def test_identity_layers_in_multipass_chains(engine, oracle, q):
+    """gamma == 0 (no phase, statevector.hpp:149) and beta == 0 (identity mixer, :193) in
+    a middle layer: the streaming passes skip those tiles (the refill path without work)."""
+    e = oracle.generate_er(q, 0.3, q + 1)
+    for g, b in [([0.7, 0.0, 1.1], [0.3, 0.0, 0.9]), ([0.0, 0.5], [0.0, 0.4])]:
+        a0, x0 = oracle.run_ansatz(q, e, g, b)
+        a1, x1 = engine.run_ansatz(q, e, g, b)
+        assert np.array_equal(a1, a0) and x1 == x0
