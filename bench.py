@@ -225,6 +225,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--report", default="",
+                    help="also write the run as an ExperimentReport JSON v1 (report.hpp) with a "
+                         "'gpu' section to this path")
     ap.add_argument("--profile-stride", type=int, default=PROFILE_STRIDE,
                     help="CUDA-event sampling of 1 launch in N during the timed region (0: off)")
     args = ap.parse_args()
@@ -431,6 +434,19 @@ def main():
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": "unavailable", "sample": str(ex)}
     print(json.dumps(line), flush=True)
+    if args.report and rep is not None:
+        from paper_2603_26232_b200.report import emit_report, experiment_report
+        doc = experiment_report(
+            rep, n=w["n"], edges=len(edges), cfg=dict(cfg, shard_count=world), generated=True,
+            p=w.get("p_edge", 0.0), graph_seed=w["seed"],
+            gpu={"device": torch.cuda.get_device_name(local), "n_gpus": world,
+                 "precision": "fp64", "evals_per_s": line["value"],
+                 "e2e_evals_per_s": e2e["value"], "ms_per_step": line["ms_per_step"],
+                 "roofline": {"kernel": roofline["kernel"], "hbm_frac": roofline["frac"],
+                              "fp64_frac": roofline["fp64"]["frac"]},
+                 "clocks": clk})
+        with open(args.report, "w") as f:
+            f.write(emit_report(doc))
     if world > 1:
         dist.destroy_process_group()
     return 0
