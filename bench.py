@@ -202,7 +202,7 @@ def run_reference_arm(args, w):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(totals) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
         "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
                    "qubit_cap": w["qubit_cap"], "layers": w["layers"], "top_k": w["top_k"],
                    "budget": w["budget"], "parallelism": f"cpu x{cores} threads"},
@@ -225,6 +225,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="64: exact fp64 (the parity path, default); 32: optional fp32 mode (1e-4)")
     ap.add_argument("--report", default="",
                     help="also write the run as an ExperimentReport JSON v1 (report.hpp) with a "
                          "'gpu' section to this path")
@@ -246,6 +248,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     eng = Engine(local)
+    eng.set_precision(args.precision)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     edges = workload_graph(w)
     cfg = dict(qubit_cap=w["qubit_cap"], top_k=w["top_k"], layers=w["layers"],
@@ -411,7 +414,7 @@ def main():
         "metric": METRIC, "value": evals_per_step / sec_per_step, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
         "data": "synthetic (graph.hpp:146 ER generator restated in qc_generate_er)",
         "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
                    "qubit_cap": w["qubit_cap"], "subgraphs": n_sub, "layers": w["layers"],
@@ -440,7 +443,7 @@ def main():
             rep, n=w["n"], edges=len(edges), cfg=dict(cfg, shard_count=world), generated=True,
             p=w.get("p_edge", 0.0), graph_seed=w["seed"],
             gpu={"device": torch.cuda.get_device_name(local), "n_gpus": world,
-                 "precision": "fp64", "evals_per_s": line["value"],
+                 "precision": f"fp{args.precision}", "evals_per_s": line["value"],
                  "e2e_evals_per_s": e2e["value"], "ms_per_step": line["ms_per_step"],
                  "roofline": {"kernel": roofline["kernel"], "hbm_frac": roofline["frac"],
                               "fp64_frac": roofline["fp64"]["frac"]},

@@ -172,6 +172,11 @@ int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
  * 2 pass_low, 3 pass_high, 4 blocksum, 5 finalsum, 6 topk, 7 merge_tables,
  * 8 merge_search, 9 merge_other), the launch count, summed device ms and summed
  * algorithmic bytes since the last qc_engine_profile call. */
+/* Arithmetic of the batched solve / eval paths (qc_solve_batch, qc_eval_batch, the
+ * pipeline): 64 = exact fp64, bit-identical to the reference (default); 32 = optional fp32
+ * mode (float amplitudes, FMA; expectations within 1e-4 relative). The statevector-level
+ * calls (qc_run_ansatz, qc_apply_*) always use fp64. Config error for other values. */
+int qc_engine_set_precision(qc_engine* e, int bits);
 int qc_engine_profile(qc_engine* e, int on);
 int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
                            double* bytes);

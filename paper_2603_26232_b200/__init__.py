@@ -338,6 +338,10 @@ class Engine:
     def launches(self) -> int:
         return int(self.lib.qc_engine_launches(self._h))
 
+    def set_precision(self, bits: int):
+        """64: exact fp64 (default); 32: optional fp32 mode for solve/eval (1e-4)."""
+        self._call("qc_engine_set_precision", C.c_int(bits))
+
     def set_memory_budget(self, nbytes: int):
         self._call("qc_engine_set_memory_budget", C.c_uint64(nbytes))
 

@@ -202,9 +202,10 @@ size_t qc_engine::max_slots(int Q, bool onchip) const {
     return s;
 }
 
-double2* qc_engine::slot_state(int q, bool sym, int k) {
+double2* qc_engine::slot_state(int q, bool sym, int k, bool fp32) {
     const int Q = sym ? q - 1 : q;
-    return static_cast<double2*>(states.p) + (static_cast<size_t>(k) << Q);
+    return reinterpret_cast<double2*>(static_cast<char*>(states.p) +
+                                      (static_cast<size_t>(k) << Q) * (fp32 ? 8 : 16));
 }
 
 void qc_engine::sync() { QC_CUDA(cudaStreamSynchronize(stream)); }
@@ -247,9 +248,12 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     const DevGraph& g0 = dg[static_cast<size_t>(pts[0].g)];
     const ChainPlan plan = plan_chain(g0.q, g0.sym);
     const size_t N = size_t{1} << plan.Q;
-    auto* st = static_cast<double2*>(states.p) + slot0 * N;
-    double* fb = nullptr;
-    if (!plan.onchip && (flags & F_EXPECT)) fb = static_cast<double*>(fbuf.p) + slot0 * N;
+    // fp32 mode: float2 amplitudes / float f(z) packed at half the fp64 stride
+    const bool fp32 = flags & F_FP32;
+    const size_t ab = fp32 ? 8 : 16, fbb = fp32 ? 4 : 8;
+    char* st = static_cast<char*>(states.p) + slot0 * N * ab;
+    char* fb = nullptr;
+    if (!plan.onchip && (flags & F_EXPECT)) fb = static_cast<char*>(fbuf.p) + slot0 * N * fbb;
     const size_t pps = partials_per_slot(plan);
     auto* part = static_cast<double*>(partials.p) + slot0 * pps;
     auto* tick = static_cast<unsigned*>(tickets.p) + slot0;
@@ -268,7 +272,8 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     const size_t o_lut =
         (o_lp + static_cast<size_t>(n) * static_cast<size_t>(std::max(p, 1)) * sizeof(LayerParam) + 255) &
         ~size_t{255};
-    const size_t bytes = o_lut + lut_total * 16;
+    const size_t lut_entry = fp32 ? 8 : 16;  // double2 (exact) or float2 LUT entries
+    const size_t bytes = o_lut + lut_total * lut_entry;
     char* h = static_cast<char*>(ctx.hstage.get(bytes));
     char* d = static_cast<char*>(ctx.dstage.get(bytes));
     auto* hs = reinterpret_cast<SlotDesc*>(h);
@@ -282,8 +287,8 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     for (int k = 0; k < n; ++k) {
         const DevGraph& dgk = dg[static_cast<size_t>(pts[k].g)];
         SlotDesc& s = hs[k];
-        s.state = st + static_cast<size_t>(k) * N;
-        s.fbuf = fb ? fb + static_cast<size_t>(k) * N : nullptr;
+        s.state = reinterpret_cast<double2*>(st + static_cast<size_t>(k) * N * ab);
+        s.fbuf = fb ? reinterpret_cast<double*>(fb + static_cast<size_t>(k) * N * fbb) : nullptr;
         s.lev = dgk.unit_cost ? nullptr : dgk.lev;
         s.val = dgk.unit_cost ? nullptr : dgk.val;
         s.amp0 = amp0;
@@ -306,13 +311,22 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             L.pad = 0;
             if (L.phase && dgk.integral && !dgk.unit_cost) {
                 // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c)
-                double* dst = hlut + 2 * lut_pos;
-                for (int c = 0; c < dgk.lut_len; ++c) {
-                    const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
-                    dst[2 * c] = z.real();
-                    dst[2 * c + 1] = z.imag();
+                if (fp32) {
+                    float* dst = reinterpret_cast<float*>(h + o_lut) + 2 * lut_pos;
+                    for (int c = 0; c < dgk.lut_len; ++c) {
+                        const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
+                        dst[2 * c] = static_cast<float>(z.real());
+                        dst[2 * c + 1] = static_cast<float>(z.imag());
+                    }
+                } else {
+                    double* dst = hlut + 2 * lut_pos;
+                    for (int c = 0; c < dgk.lut_len; ++c) {
+                        const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
+                        dst[2 * c] = z.real();
+                        dst[2 * c + 1] = z.imag();
+                    }
                 }
-                L.lut = reinterpret_cast<const double2*>(d + o_lut) + lut_pos;
+                L.lut = reinterpret_cast<const double2*>(d + o_lut + lut_pos * lut_entry);
                 L.lut_len = dgk.lut_len;
                 lut_pos += static_cast<size_t>(dgk.lut_len);
             }
@@ -320,7 +334,8 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     }
     h2d_copy(d, h, bytes, cs);
     launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
-                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags, fb,
+                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
+                             reinterpret_cast<double*>(fb),
                              part, tick, od, cs, &stats, &prof);
     if (flags & F_EXPECT) {
         auto* ho = static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8));
@@ -362,7 +377,7 @@ void qc_engine::eval(const std::vector<DevGraph>& dg, const std::vector<EvalPoin
             buf.clear();
             for (size_t k = b; k < e; ++k) buf.push_back(pts[static_cast<size_t>(idx[k])]);
             res.assign(buf.size(), 0.0);
-            eval_chunk(dg, buf.data(), static_cast<int>(buf.size()), p, F_INIT | F_EXPECT,
+            eval_chunk(dg, buf.data(), static_cast<int>(buf.size()), p, F_INIT | F_EXPECT | fp_flag(),
                        res.data());
             for (size_t k = b; k < e; ++k) out[idx[k]] = res[k - b];
         }
@@ -433,7 +448,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                 inflight[c] = !pts[c].empty();
                 if (inflight[c])
                     e->enqueue_chunk(dg, pts[c].data(), static_cast<int>(pts[c].size()), p,
-                                     F_INIT | F_EXPECT, c * per, ctx(c));
+                                     F_INIT | F_EXPECT | e->fp_flag(), c * per, ctx(c));
             };
             for (size_t c = 0; c < nchunks; ++c) launch(c);
             // completion-order service: whichever chunk's step finished is told/asked and
@@ -543,7 +558,8 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
             const size_t end = std::min(ids.size(), b + cap);
             std::vector<EvalPoint> pts;
             for (size_t k = b; k < end; ++k) pts.push_back({static_cast<int>(ids[k]), best[ids[k]].params.data()});
-            e->eval_chunk(dg, pts.data(), static_cast<int>(pts.size()), p, F_INIT | F_STATE_OUT,
+            e->eval_chunk(dg, pts.data(), static_cast<int>(pts.size()), p,
+                          F_INIT | F_STATE_OUT | e->fp_flag(),
                           nullptr);
             for (size_t k = b; k < end; ++k) {
                 const size_t i = ids[k];
@@ -554,9 +570,10 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
                 char* ob = static_cast<char*>(e->topk_out.get(static_cast<size_t>(K) * 12 + 64));
                 auto* d_bits = reinterpret_cast<uint32_t*>(ob);
                 auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(K) * 4 + 15) & ~size_t{15}));
-                e->launches += launch_topk(e->slot_state(q, dg[i].sym, static_cast<int>(k - b)), q,
-                                           dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream,
-                                           &e->prof);
+                e->launches += launch_topk(e->slot_state(q, dg[i].sym, static_cast<int>(k - b),
+                                                         e->precision == 32),
+                                           q, dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream,
+                                           &e->prof, e->precision == 32);
                 SolveOut& r = out[i];
                 r.width = q;
                 r.folded = fold;
@@ -678,6 +695,14 @@ void qc_engine_destroy(qc_engine* e) {
     }
     cudaStreamDestroy(e->stream);
     delete e;
+}
+
+int qc_engine_set_precision(qc_engine* e, int bits) {
+    return guarded([&] {
+        check_engine(e);
+        if (bits != 64 && bits != 32) config_error("precision must be 64 (exact) or 32 (fp32 mode)");
+        e->precision = bits;
+    });
 }
 
 int qc_engine_profile(qc_engine* e, int on) {

@@ -114,7 +114,11 @@ struct qc_engine {
     qcg::ChunkCtx sync_ctx;
     void eval(const std::vector<qcg::DevGraph>& dg, const std::vector<qcg::EvalPoint>& pts, int p,
               double* out);
-    double2* slot_state(int q, bool sym, int k);
+    double2* slot_state(int q, bool sym, int k, bool fp32 = false);
+    // 64: the exact fp64 path (default, bit-identical to the reference); 32: optional fp32
+    // mode for the batched solve/eval paths (statevector-level calls stay fp64)
+    int precision = 64;
+    uint32_t fp_flag() const { return precision == 32 ? qcg::F_FP32 : 0u; }
     void sync();
 };
 

@@ -61,6 +61,7 @@ enum : uint32_t {
     F_EXPECT = 2u,      // compute the blocked expectation after the last layer
     F_STATE_OUT = 4u,   // final state must be written back
     F_SYM = 8u,         // half-state storage (complement symmetry), else full state
+    F_FP32 = 64u,       // optional fp32 mode: float2 amplitudes, float f(z), fp32 LUTs (1e-4)
 };
 
 // One high (gather) pass: 3 column bits (0,1,2) + kHighBits tile bits.
@@ -202,7 +203,9 @@ void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
 // Top-K over the classes of one state (qc_topk.cu). Writes k (bits, prob) pairs,
 // ordered by (prob desc, lex asc) (qaoa.hpp:179-182). d_scratch sized by topk_scratch_bytes.
 size_t topk_scratch_bytes(int q, bool fold, int k);
+// fp32: d_state holds float2 amplitudes (F_FP32 chains)
 int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
-                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof = nullptr);
+                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof = nullptr,
+                bool fp32 = false);
 
 }  // namespace qcg

@@ -30,6 +30,7 @@
 #include <string>
 #include <cstdint>
 
+#include "qc_amp.cuh"
 #include "qc_internal.hpp"
 
 namespace qcg {
@@ -225,6 +226,110 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const SlotDesc* __res
     }
     if (flags & F_STATE_OUT)
         for (uint32_t e = tid; e < N; e += kOnchipThreads) S.state[e] = sa[e];
+}
+
+// ---------------------------------------------------------------------------
+// Optional fp32 mode (F_FP32, 1e-4): float2 amplitudes, float f(z). Same schedule as the
+// fp64 kernels (phase, RX targets ascending, mirror last); sums accumulate in double.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kOnchipThreads) k_onchip_f32(const SlotDesc* __restrict__ slots,
+                                                             const LayerParam* __restrict__ lp,
+                                                             int p, int Q, uint32_t flags,
+                                                             double* __restrict__ out) {
+    extern __shared__ float2 smemf[];
+    using A = Amp<float2>;
+    const uint32_t N = 1u << Q;
+    float2* sa = smemf;
+    __shared__ double red[kOnchipThreads / 32];
+    const SlotDesc S = slots[blockIdx.x];
+    float2* gst = reinterpret_cast<float2*>(S.state);
+    const bool sym = flags & F_SYM;
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t e = tid; e < N; e += kOnchipThreads)
+        sa[e] = (flags & F_INIT) ? make_float2(static_cast<float>(S.amp0), 0.f) : gst[e];
+    for (int l = 0; l < p; ++l) {
+        const LayerParam L = lp[S.layer_base + l];
+        const float c = static_cast<float>(L.c), sn = static_cast<float>(L.s);
+        if (L.phase) {
+            const float2* lut = reinterpret_cast<const float2*>(L.lut);
+            for (uint32_t e = tid; e < N; e += kOnchipThreads) {
+                if (S.lev) {
+                    sa[e] = A::cmul(sa[e], lut[S.lev[e]]);
+                } else {
+                    double s_, c_;
+                    sincos(-L.gamma * S.val[e], &s_, &c_);
+                    sa[e] = A::cmul(sa[e], make_float2(static_cast<float>(c_), static_cast<float>(s_)));
+                }
+            }
+        }
+        __syncthreads();
+        if (!L.mix) continue;
+        for (int t = 0; t < Q; ++t) {
+            const uint32_t half = 1u << t, lo = half - 1u;
+            for (uint32_t k = tid; k < N / 2; k += kOnchipThreads) {
+                const uint32_t i = ((k & ~lo) << 1) | (k & lo);
+                A::rx(sa[i], sa[i | half], c, sn);
+            }
+            __syncthreads();
+        }
+        if (sym) {
+            for (uint32_t k = tid; k < N / 2; k += kOnchipThreads) A::rx(sa[k], sa[(N - 1u) ^ k], c, sn);
+            __syncthreads();
+        }
+    }
+    if (flags & F_EXPECT) {
+        double acc = 0.0;
+        for (uint32_t e = tid; e < N; e += kOnchipThreads) {
+            const double cst = S.lev ? static_cast<double>(S.lev[e]) : (S.val ? S.val[e] : 1.0);
+            acc += static_cast<double>(A::nrm(sa[e])) * cst;
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kOnchipThreads / 32; ++w) t += red[w];
+            out[blockIdx.x] = sym ? 2.0 * t : t;
+        }
+    }
+    if (flags & F_STATE_OUT)
+        for (uint32_t e = tid; e < N; e += kOnchipThreads) gst[e] = sa[e];
+}
+
+// fp32 expectation: one CTA per stored 4096-block sums float f in double; the last CTA of
+// a slot adds the partials in block order (x2 for the mirror half in SYM storage).
+constexpr int kFsumThreads = 256;
+__global__ void __launch_bounds__(kFsumThreads) k_fsum_f32(const float* __restrict__ f, int Q, int sym,
+                                                         double* __restrict__ partials,
+                                                         unsigned* __restrict__ tickets,
+                                                         double* __restrict__ out) {
+    __shared__ double red[kFsumThreads / 32];
+    const int nbl = 1 << (Q - 12);
+    const int slot = blockIdx.x / nbl, b = blockIdx.x % nbl;
+    const float4* src = reinterpret_cast<const float4*>(f + (static_cast<size_t>(slot) << Q) +
+                                                        static_cast<size_t>(b) * kBlock);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < kBlock / 4; i += kFsumThreads) {
+        const float4 v = __ldcg(src + i);
+        acc += (static_cast<double>(v.x) + v.y) + (static_cast<double>(v.z) + v.w);
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kFsumThreads / 32; ++w) t += red[w];
+        double* pp = partials + static_cast<size_t>(slot) * nbl;
+        pp[b] = t;
+        __threadfence();
+        if (atomicAdd(&tickets[slot], 1u) == static_cast<unsigned>(nbl - 1)) {
+            __threadfence();
+            double total = 0.0;
+            for (int k = 0; k < nbl; ++k) total += __ldcg(pp + k);
+            out[slot] = sym ? 2.0 * total : total;
+            tickets[slot] = 0u;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -673,6 +778,21 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     auto cnt = [&](const std::vector<int>* v, int l) {
         return (stats && v && l < static_cast<int>(v->size())) ? (*v)[static_cast<size_t>(l)] : n_slots;
     };
+    const bool fp32 = flags & F_FP32;
+    if (plan.onchip && fp32) {
+        const size_t smem = (size_t{1} << Q) * sizeof(float2);
+        static bool attr32 = false;
+        if (!attr32) {
+            QC_CUDA(cudaFuncSetAttribute(k_onchip_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (1 << 12) * 8));
+            attr32 = true;
+        }
+        if (prof) prof->begin(K_ONCHIP, 0.0, stream);
+        k_onchip_f32<<<n_slots, kOnchipThreads, smem, stream>>>(d_slots, d_lp, p, Q, flags | symf, d_out);
+        if (prof) prof->end(stream);
+        QC_CUDA(cudaGetLastError());
+        return 1;
+    }
     if (plan.onchip) {
         const size_t Ns = size_t{1} << Q;
         const size_t smem = Ns * sizeof(double2) + ((flags & F_EXPECT) ? Ns * sizeof(double) : 0);
@@ -724,7 +844,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         if (v3)
             k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         else
-            launch_pass_a4(d_slots, d_lp, l, Q, fa, n_slots, stream, pdl_ok && l > 0);
+            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & F_FP32), n_slots, stream, pdl_ok && l > 0);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -746,12 +866,21 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                 k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
                     d_slots, d_lp, l, Q, plan.high[h], fh);
             else
-                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh, n_slots, stream, pdl_ok);
+                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & F_FP32), n_slots, stream, pdl_ok);
             if (prof) prof->end(stream);
             ++launches;
         }
     }
     QC_CUDA(cudaGetLastError());
+    if ((flags & F_EXPECT) && fp32) {
+        const int nbl = 1 << (Q - 12);
+        if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 4.0, stream);
+        k_fsum_f32<<<static_cast<unsigned>(n_slots * nbl), kFsumThreads, 0, stream>>>(
+            reinterpret_cast<const float*>(d_fbuf), Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+        if (prof) prof->end(stream);
+        QC_CUDA(cudaGetLastError());
+        return launches + 1;
+    }
     if (flags & F_EXPECT) {
         const int nbl = 1 << (Q - 12);
         const int bpw = std::min(32, nbl);

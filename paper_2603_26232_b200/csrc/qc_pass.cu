@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "qc_amp.cuh"
 #include "qc_internal.hpp"
 
 namespace qcg {
@@ -65,11 +66,7 @@ static_assert(kSmem <= 232448, "shared memory budget");
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ uint32_t sw4(uint32_t e) { return e ^ ((e >> 4) & 7u); }
 
-__device__ __forceinline__ void cpa16(uint32_t s, const void* g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
-}
 __device__ __forceinline__ void cpa_arrive(uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
@@ -95,41 +92,6 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 
 __device__ __forceinline__ void grp_sync(uint32_t g) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(g + 1u), "n"(kGT) : "memory");
-}
-
-// exact fp64 blocks (same as qc_kernels.cu)
-__device__ __forceinline__ double2 cmul(double2 a, double2 l) {
-    return make_double2(__dsub_rn(__dmul_rn(a.x, l.x), __dmul_rn(a.y, l.y)),
-                        __dadd_rn(__dmul_rn(a.x, l.y), __dmul_rn(a.y, l.x)));
-}
-__device__ __forceinline__ void rx(double2& a0, double2& a1, double c, double s) {
-    const double2 t0 = a0, t1 = a1;
-    a0.x = __dadd_rn(__dmul_rn(c, t0.x), __dmul_rn(s, t1.y));
-    a0.y = __dsub_rn(__dmul_rn(c, t0.y), __dmul_rn(s, t1.x));
-    a1.x = __dadd_rn(__dmul_rn(s, t0.y), __dmul_rn(c, t1.x));
-    a1.y = __dsub_rn(__dmul_rn(c, t1.y), __dmul_rn(s, t0.x));
-}
-__device__ __forceinline__ double nrm(double2 a) {
-    return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
-}
-
-// fractional weights: std::polar(1, -gamma*val) (device sincos), out of line so the
-// integral path keeps its registers
-__device__ __noinline__ double2 phase_frac(double2 v, double gamma, double val) {
-    double sn, cs;
-    sincos(__dmul_rn(-gamma, val), &sn, &cs);
-    return cmul(v, make_double2(cs, sn));
-}
-
-// RX on local bits [B0, B0+NB) of a[16] (ascending)
-template <int B0, int NB>
-__device__ __forceinline__ void rx_local(double2 (&a)[16], double c, double s) {
-#pragma unroll
-    for (int b = B0; b < B0 + NB; ++b) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            if (!(j & (1 << b))) rx(a[j], a[j | (1 << b)], c, s);
-    }
 }
 
 __device__ __forceinline__ void tile_range(uint32_t total, uint32_t& t0, int& cnt) {
@@ -176,6 +138,7 @@ __device__ __forceinline__ void ring_init(unsigned char* sm) {
 // pass A: tile = 4096 contiguous stored amplitudes; [|+> init] + phase + RX 0..11.
 // Rounds: bits 0-3 (e = gt*16 + j), bits 4-7, bits 8-11 (e = j*256 + gt, coalesced store).
 // ---------------------------------------------------------------------------
+template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_a(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
              int Q, uint32_t flags, uint32_t total_tiles) {
@@ -183,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
+    using S = typename Amp<V>::S;
     const bool init = flags & F_INIT;
     uint32_t t0;
     int cnt;
@@ -209,10 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (init || d.phase || d.mix) {
             if (!init) {
                 const uint32_t sb = su32(sm + s * kStageAmpBytes);
-                const double2* src = d.state + base + gt;
-                const uint32_t d0 = sb + sw4(gt) * 16u;  // sw4(gt + 256 i) = sw4(gt) + 256 i
+                const V* src = reinterpret_cast<const V*>(d.state) + base + gt;
+                const uint32_t d0 = sb + sw<V>(gt) * Amp<V>::kBytes;  // sw(gt + 256 i) = sw(gt) + 256 i
 #pragma unroll
-                for (int i = 0; i < 16; ++i) cpa16(d0 + i * (kGT * 16u), src + kGT * i);
+                for (int i = 0; i < 16; ++i) Amp<V>::cpa(d0 + i * (kGT * Amp<V>::kBytes), src + kGT * i);
                 any = true;
             }
             if (d.phase && d.lev) {
@@ -238,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(1);
     }
 
-    double2* slut = reinterpret_cast<double2*>(sm + kOffLut) + g * kLutCap;
+    V* slut = reinterpret_cast<V*>(sm + kOffLut) + g * kLutCap;
     int lut_owner = -1;  // slot whose LUT slut holds
     for (int k = static_cast<int>(g); k < cnt; k += 2) {
         const int s = k % kStages;
@@ -249,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool lut_sm = use_lev && d.lut_len <= kLutCap;
         if (lut_sm && lut_owner != d.key) {
             // every thread of the group is past the previous tile's phase (round-0) reads
-            const double2* lsrc = d.lut;
+            const V* lsrc = reinterpret_cast<const V*>(d.lut);  // host-staged V entries
             for (int i = static_cast<int>(gt); i < d.lut_len; i += kGT) slut[i] = lsrc[i];
             lut_owner = d.key;
             grp_sync(g);
@@ -263,16 +227,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;  // identity layer: memory already holds the result
         }
         const uint32_t base = (t & tmask) << 12;
-        double2* st = reinterpret_cast<double2*>(sm + s * kStageAmpBytes);
-        const double c = d.c, sn = d.s;
+        V* st = reinterpret_cast<V*>(sm + s * kStageAmpBytes);
+        const S c = static_cast<S>(d.c), sn = static_cast<S>(d.s);
         const bool mix = d.mix;
-        double2 a[16];
+        V a[16];
         // round 0: bits 0-3, phase first
         {
             const uint4* lv = reinterpret_cast<const uint4*>(sm + kOffLev + s * 8192u) + gt * 2u;
-            const double2* lutp = lut_sm ? slut : d.lut;
+            const V* lutp = lut_sm ? slut : reinterpret_cast<const V*>(d.lut);
             const bool phase = d.phase;
-            const double amp0 = d.amp0;
+            const S amp0 = static_cast<S>(d.amp0);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
@@ -280,47 +244,47 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int jj = 0; jj < 8; ++jj) {
                     const int j = h * 8 + jj;
                     const uint32_t e = gt * 16u + j;
-                    double2 v = init ? make_double2(amp0, 0.0) : st[sw4(e)];
+                    V v = init ? Amp<V>::mk(amp0, S(0)) : st[sw<V>(e)];
                     if (phase) {
                         if (use_lev) {
                             const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
                                                 : (jj >> 1) == 2 ? l4.z : l4.w;
-                            v = cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
+                            v = Amp<V>::cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
                         } else {
-                            v = phase_frac(v, d.gamma, d.val[base + e]);
+                            v = phase_frac<V>(v, d.gamma, d.val[base + e]);
                         }
                     }
                     a[j] = v;
                 }
             }
-            if (mix) rx_local<0, 4>(a, c, sn);
+            if (mix) rx_local<V, 0, 4>(a, c, sn);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st[sw4(gt * 16u + j)] = a[j];
+            for (int j = 0; j < 16; ++j) st[sw<V>(gt * 16u + j)] = a[j];
         }
         grp_sync(g);
         // round 1: bits 4-7, e = (gt>>4)<<8 | j<<4 | gt&15
         {
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) a[j] = st[sw4(r | (j << 4))];
-            if (mix) rx_local<0, 4>(a, c, sn);
+            for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(r | (j << 4))];
+            if (mix) rx_local<V, 0, 4>(a, c, sn);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st[sw4(r | (j << 4))] = a[j];
+            for (int j = 0; j < 16; ++j) st[sw<V>(r | (j << 4))] = a[j];
         }
         grp_sync(g);
         // round 2: bits 8-11, e = j<<8 | gt
-        const double2* st2 = st + sw4(gt);  // sw4(j<<8 | gt) = j<<8 | sw4(gt)
+        const V* st2 = st + sw<V>(gt);  // sw(j<<8 | gt) = j<<8 | sw(gt)
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = st2[j << 8];
-        double2* __restrict__ dst = d.state + base;
+        V* __restrict__ dst = reinterpret_cast<V*>(d.state) + base;
         grp_sync(g);  // the whole group is done with this stage: refill it
         issue(k + kStages);
         // last target (bit 11 = local bit 3) pair by pair, each pair stored as soon as it
         // is final: spreads the 64 KB of stores over the round instead of one burst
-        if (mix) rx_local<0, 3>(a, c, sn);
+        if (mix) rx_local<V, 0, 3>(a, c, sn);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            if (mix) rx(a[j], a[j + 8], c, sn);
+            if (mix) Amp<V>::rx(a[j], a[j + 8], c, sn);
             dst[(j << 8) | gt] = a[j];
             dst[((j + 8) << 8) | gt] = a[j + 8];
         }
@@ -356,14 +320,15 @@ __device__ __forceinline__ uint32_t deposit4(uint32_t v, uint32_t mask) {
 }
 
 // pair ops on local bits of a[16]: local bit b -> gather bit G0 + b (kind != 0 => op)
-template <int G0, int NB>
-__device__ __forceinline__ void ops_local(double2 (&a)[16], const HighPass& hp, double c, double s) {
+template <typename V, int G0, int NB>
+__device__ __forceinline__ void ops_local(V (&a)[16], const HighPass& hp, typename Amp<V>::S c,
+                                          typename Amp<V>::S s) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         if (hp.kind[G0 + b] == 0) continue;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            if (!(j & (1 << b))) rx(a[j], a[j | (1 << b)], c, s);
+            if (!(j & (1 << b))) Amp<V>::rx(a[j], a[j | (1 << b)], c, s);
     }
 }
 
@@ -375,6 +340,7 @@ __device__ __forceinline__ uint32_t gb_local(int j) {
     return (static_cast<uint32_t>(j >> 1) & 7u) | (static_cast<uint32_t>(j & 1) << 8);
 }
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_b(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
              int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles) {
@@ -382,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
+    using S = typename Amp<V>::S;
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
     uint32_t t0;
@@ -411,11 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool any = false;
         if (d.mix || fout) {
             const uint32_t xb = deposit4(t & tmask, hp.freemask);
-            const uint32_t sb = su32(sm + s * kStageAmpBytes) + sw4(gt) * 16u;
+            const uint32_t sb = su32(sm + s * kStageAmpBytes) + sw<V>(gt) * Amp<V>::kBytes;
             const uint32_t x = (xb | w) ^ tx_issue;
+            const V* gs = reinterpret_cast<const V*>(d.state);
 #pragma unroll
             for (int i = 0; i < 16; ++i)  // unit e = gt + 256 i: gb = gt>>3 | i<<5
-                cpa16(sb + i * (kGT * 16u), d.state + (x ^ hx(hp, static_cast<uint32_t>(i) << 5)));
+                Amp<V>::cpa(sb + i * (kGT * Amp<V>::kBytes), gs + (x ^ hx(hp, static_cast<uint32_t>(i) << 5)));
             if (fout && d.lev) {
                 const uint32_t lb = su32(sm + kOffLev + s * 8192u);
 #pragma unroll
@@ -456,14 +424,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int nrr = mix ? nr : 1;  // no mixer: only f(z) to emit
         const uint32_t xb = sxb[s] | w;
-        const double c = d.c, sn = d.s;
-        double2* st = reinterpret_cast<double2*>(sm + s * kStageAmpBytes);
+        const S c = static_cast<S>(d.c), sn = static_cast<S>(d.s);
+        V* st = reinterpret_cast<V*>(sm + s * kStageAmpBytes);
         const uint16_t* slev = reinterpret_cast<const uint16_t*>(sm + kOffLev + s * 8192u);
-        double2* const gstate = d.state;
-        double* const gf = d.fbuf;
+        V* const gstate = reinterpret_cast<V*>(d.state);
+        S* const gf = reinterpret_cast<S*>(d.fbuf);  // f(z) in the amplitude precision
         const uint16_t* const glev = d.lev;
         const double* const gval = d.val;
-        double2 a[16];
+        V a[16];
         // tile index of amp j in round R
         auto e_of = [&](auto R, int j) -> uint32_t {
             if constexpr (decltype(R)::value == 0)
@@ -486,12 +454,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t gidx = xt ^ hx(hp, gb_local<r>(j));
                 if (sout) __stcs(gstate + gidx, a[j]);
                 if (fout) {
-                    double cst;
+                    S cst;
                     if (glev)
-                        cst = static_cast<double>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
+                        cst = static_cast<S>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
                     else
-                        cst = gval ? gval[gidx] : 1.0;
-                    gf[gidx] = __dmul_rn(nrm(a[j]), cst);  // stays in L2 for k_blocksum
+                        cst = static_cast<S>(gval ? gval[gidx] : 1.0);
+                    gf[gidx] = Amp<V>::mul(Amp<V>::nrm(a[j]), cst);  // stays in L2 for k_blocksum
                 }
             }
         };
@@ -509,49 +477,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         using R2 = std::integral_constant<int, 2>;
         // round 0: gather bits 0-3 local
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R0{}, j))];
-        if (mix) ops_local<0, 4>(a, hp, c, sn);
+        for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R0{}, j))];
+        if (mix) ops_local<V, 0, 4>(a, hp, c, sn);
         if (nrr == 1) {
             finish(R0{});
             continue;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) st[sw4(e_of(R0{}, j))] = a[j];
+        for (int j = 0; j < 16; ++j) st[sw<V>(e_of(R0{}, j))] = a[j];
         grp_sync(g);
         // round 1: gather bits 4-7 local
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R1{}, j))];
-        ops_local<4, 4>(a, hp, c, sn);
+        for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R1{}, j))];
+        ops_local<V, 4, 4>(a, hp, c, sn);
         if (nrr == 2) {
             finish(R1{});
             continue;
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) st[sw4(e_of(R1{}, j))] = a[j];
+        for (int j = 0; j < 16; ++j) st[sw<V>(e_of(R1{}, j))] = a[j];
         grp_sync(g);
         // round 2: gather bit 8 local (j bit 0); j bits 1-3 carry gather bits 0-2
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = st[sw4(e_of(R2{}, j))];
-        ops_local<8, 1>(a, hp, c, sn);
+        for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R2{}, j))];
+        ops_local<V, 8, 1>(a, hp, c, sn);
         finish(R2{});
     }
 }
 
 }  // namespace v4
 
-size_t pass4_smem() { return v4::kSmem; }
 
 namespace {
+template <typename V>
+void set_attrs() {
+    QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(v4::kSmem)));
+    QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(v4::kSmem)));
+}
 int sm_count() {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         QC_CUDA(cudaGetDevice(&dev));
         QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(v4::kSmem)));
-        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(v4::kSmem)));
+        set_attrs<double2>();
+        set_attrs<float2>();
     }
     return sms;
 }
@@ -560,17 +532,23 @@ int sm_count() {
 int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
 }  // namespace
 
+size_t pass4_smem() { return v4::kSmem; }
+
 int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
                    int n_slots, cudaStream_t stream, bool pdl) {
     const int sms = sm_count();
+    const bool fp32 = flags & F_FP32;
     int launches = 0;
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
         const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
-        launch_ex(v4::k_pass_a, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream, pdl || s0 > 0,
-                  d_slots + s0, d_lp, layer, Q, flags, tiles);
-        QC_CUDA(cudaGetLastError());
+        if (fp32)
+            launch_ex(v4::k_pass_a<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles);
+        else
+            launch_ex(v4::k_pass_a<double2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles);
         ++launches;
     }
     return launches;
@@ -579,14 +557,18 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
                    const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream, bool pdl) {
     const int sms = sm_count();
+    const bool fp32 = flags & F_FP32;
     int launches = 0;
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
         const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
-        v4::k_pass_b<<<grid, v4::kThreads, v4::kSmem, stream>>>(d_slots + s0, d_lp, layer, Q, hp,
-                                                               flags, tiles);
-        QC_CUDA(cudaGetLastError());
+        if (fp32)
+            launch_ex(v4::k_pass_b<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags, tiles);
+        else
+            launch_ex(v4::k_pass_b<double2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags, tiles);
         ++launches;
     }
     return launches;

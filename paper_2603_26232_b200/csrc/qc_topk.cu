@@ -38,10 +38,14 @@ __device__ __forceinline__ bool key_gt(const Key& a, const Key& b) {
 __device__ __forceinline__ double norm_rn2(double2 a) {
     return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
 }
+__device__ __forceinline__ double norm_rn2(float2 a) {  // fp32 mode: exact products in double
+    return norm_rn2(make_double2(a.x, a.y));
+}
 
 // class c -> key
-__device__ __forceinline__ Key class_key(const double2* __restrict__ st, uint64_t c, int q,
-                                         bool sym, bool fold) {
+template <typename V>
+__device__ __forceinline__ Key class_key(const V* __restrict__ st, uint64_t c, int q, bool sym,
+                                         bool fold) {
     const uint32_t full = (q == 32) ? ~0u : ((1u << q) - 1u);
     uint32_t bits;
     double prob;
@@ -93,7 +97,8 @@ __device__ void bitonic_desc(Key* s) {
 }
 
 // Stage 1: keys from the state, chunk top-k -> out (k per chunk).
-__global__ void __launch_bounds__(kSortThreads) k_topk_state(const double2* __restrict__ st, int q,
+template <typename V>
+__global__ void __launch_bounds__(kSortThreads) k_topk_state(const V* __restrict__ st, int q,
                                                            int sym, int fold, uint64_t classes,
                                                            int k, Key* __restrict__ out) {
     __shared__ Key s[kChunk];
@@ -133,7 +138,8 @@ __global__ void __launch_bounds__(kSortThreads) k_topk_keys(const Key* __restric
 }
 
 // Global bitonic sort (descending) for K > kChunk/2.
-__global__ void k_fill_keys(const double2* __restrict__ st, int q, int sym, int fold,
+template <typename V>
+__global__ void k_fill_keys(const V* __restrict__ st, int q, int sym, int fold,
                             uint64_t classes, uint64_t padded, Key* __restrict__ keys) {
     const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (c >= padded) return;
@@ -263,8 +269,8 @@ __device__ __forceinline__ void block_select(TopList<KT>& L, int k, Key* __restr
     }
 }
 
-template <int KT>
-__global__ void __launch_bounds__(kSmallThreads) k_topk_small_state(const double2* __restrict__ st,
+template <int KT, typename V>
+__global__ void __launch_bounds__(kSmallThreads) k_topk_small_state(const V* __restrict__ st,
                                                                   int q, int sym, int fold,
                                                                   uint64_t classes, int k,
                                                                   Key* __restrict__ out) {
@@ -289,8 +295,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_topk_small_keys(const Key* __
     block_select<KT>(L, k, out);
 }
 
-template <int KT>
-int launch_small(const double2* d_state, int q, bool sym, bool fold, uint64_t classes, int k,
+template <int KT, typename V>
+int launch_small(const V* d_state, int q, bool sym, bool fold, uint64_t classes, int k,
                  Key* keys, cudaStream_t stream) {
     static int sms = 0;
     if (!sms) {
@@ -301,7 +307,7 @@ int launch_small(const double2* d_state, int q, bool sym, bool fold, uint64_t cl
     const uint64_t want = (classes + 8 * kSmallThreads - 1) / (8 * kSmallThreads);  // >= 8 per thread
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 2u * sms)));
     Key* part = keys + 1024;  // stage-1 lists (grid * k keys), final list at keys[0..k)
-    k_topk_small_state<KT><<<grid, kSmallThreads, 0, stream>>>(d_state, q, sym, fold, classes, k,
+    k_topk_small_state<KT, V><<<grid, kSmallThreads, 0, stream>>>(d_state, q, sym, fold, classes, k,
                                                               grid == 1 ? keys : part);
     if (grid > 1)
         k_topk_small_keys<KT><<<1, kSmallThreads, 0, stream>>>(part, static_cast<uint64_t>(grid) * k,
@@ -329,8 +335,9 @@ size_t topk_scratch_bytes(int q, bool fold, int k) {
     return 2 * chunks * static_cast<uint64_t>(k) * sizeof(Key) + sizeof(Key);
 }
 
-int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
-                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof) {
+template <typename V>
+int launch_topk_t(const V* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
+                  uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof) {
     const uint64_t classes = class_count(q, fold);
     const double sbytes = static_cast<double>(sym ? (uint64_t{1} << (q - 1)) : (uint64_t{1} << q)) * 16.0;
     if (prof) prof->begin(K_TOPK, sbytes, stream);
@@ -346,24 +353,24 @@ int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void*
     if (k <= 32 && !std::getenv("QCG_TOPK_SORT")) {
         const int kk = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(k), classes));
         if (k <= 1)
-            launches = launch_small<1>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<1, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         else if (k <= 2)
-            launches = launch_small<2>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<2, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         else if (k <= 4)
-            launches = launch_small<4>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<4, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         else if (k <= 8)
-            launches = launch_small<8>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<8, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         else if (k <= 16)
-            launches = launch_small<16>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<16, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         else
-            launches = launch_small<32>(d_state, q, sym, fold, classes, kk, keys, stream);
+            launches = launch_small<32, V>(d_state, q, sym, fold, classes, kk, keys, stream);
         k_emit<<<1, 32, 0, stream>>>(keys, k, d_bits, d_probs);
         QC_CUDA(cudaGetLastError());
         return launches + 1;
     }
     if (k > kChunk / 2) {
         const uint64_t n = pow2_ceil(classes);
-        k_fill_keys<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+        k_fill_keys<V><<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
             d_state, q, sym, fold, classes, n, keys);
         ++launches;
         for (uint64_t size = 2; size <= n; size <<= 1)
@@ -379,7 +386,7 @@ int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void*
     uint64_t chunks = (classes + kChunk - 1) / kChunk;
     Key* a = keys;
     Key* b = keys + chunks * static_cast<uint64_t>(k);
-    k_topk_state<<<static_cast<unsigned>(chunks), kSortThreads, 0, stream>>>(
+    k_topk_state<V><<<static_cast<unsigned>(chunks), kSortThreads, 0, stream>>>(
         d_state, q, sym, fold, classes, k, a);
     ++launches;
     uint64_t count = chunks * static_cast<uint64_t>(k);
@@ -397,6 +404,14 @@ int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void*
     k_emit<<<(k + 255) / 256, 256, 0, stream>>>(a, k, d_bits, d_probs);
     QC_CUDA(cudaGetLastError());
     return launches + 1;
+}
+
+int launch_topk(const double2* d_state, int q, bool sym, bool fold, int k, void* d_scratch,
+                uint32_t* d_bits, double* d_probs, cudaStream_t stream, Prof* prof, bool fp32) {
+    if (fp32)
+        return launch_topk_t(reinterpret_cast<const float2*>(d_state), q, sym, fold, k, d_scratch,
+                             d_bits, d_probs, stream, prof);
+    return launch_topk_t(d_state, q, sym, fold, k, d_scratch, d_bits, d_probs, stream, prof);
 }
 
 }  // namespace qcg
