@@ -580,8 +580,9 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
     extern __shared__ unsigned char sraw[];
-    unsigned char* sbase = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(sraw) + 1023) & ~uintptr_t{1023});
+    // 1024-byte aligned base by pointer arithmetic, so the compiler keeps the shared
+    // address space (LDS instead of generic LD on the chain's operand path)
+    unsigned char* sbase = sraw + ((1024u - (smem_u32(sraw) & 1023u)) & 1023u);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + kSumStages * kSumStageBytes);
     const int lane = threadIdx.x;
     const int nbl = 1 << (Q - 12);                   // stored blocks per slot
@@ -668,14 +669,27 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     }
     double* pp = partials + (size_t)slot * chains;
     if (lane < bpw) pp[desc ? 2 * nbl - 1 - (b0 + lane) : (b0 + lane)] = acc;
+    __threadfence();
     __syncwarp();
-    if (lane == 0) {
+    unsigned ticket = 0;
+    if (lane == 0) ticket = atomicAdd(&tickets[slot], 1u);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket == static_cast<unsigned>(wps - 1)) {  // last warp of this slot
         __threadfence();
-        const unsigned ticket = atomicAdd(&tickets[slot], 1u);
-        if (ticket == static_cast<unsigned>(wps - 1)) {  // last warp of this slot
-            __threadfence();
-            double total = 0.0;
-            for (int k = 0; k < chains; ++k) total = __dadd_rn(total, __ldcg(pp + k));
+        // the whole warp stages the partials (coalesced, one L2 round trip) into the
+        // chain stage it no longer needs; lane 0 then adds them in block order
+        double* sp = reinterpret_cast<double*>(sbase);
+        constexpr int kBatch = static_cast<int>(kSumStages * kSumStageBytes / sizeof(double));
+        double total = 0.0;
+        for (int k0 = 0; k0 < chains; k0 += kBatch) {  // 26 qubits: 16,384 partials
+            const int kn = min(kBatch, chains - k0);
+            for (int k = lane; k < kn; k += 32) sp[k] = __ldcg(pp + k0 + k);
+            __syncwarp();
+            if (lane == 0)
+                for (int k = 0; k < kn; ++k) total = __dadd_rn(total, sp[k]);
+            __syncwarp();
+        }
+        if (lane == 0) {
             out[slot] = total;
             tickets[slot] = 0u;
         }
