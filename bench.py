@@ -244,9 +244,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # QCG_BENCH_BACKEND=gloo exercises the multi-rank path on a box with fewer GPUs than
+    # ranks (ranks share devices, records gathered through host memory); default NCCL.
+    backend = os.environ.get("QCG_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    coll_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     eng = Engine(local)
     eng.set_precision(args.precision)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
@@ -273,8 +282,7 @@ def main():
 
         def step_value():
             # shard the QAOA stage, one NCCL all-gather of solve records, merge on rank 0
-            return solve_sharded(eng, w["n"], edges, rank, world,
-                                 device=torch.device("cuda", local), **cfg)
+            return solve_sharded(eng, w["n"], edges, rank, world, device=coll_dev, **cfg)
 
     def timed(fn, steps, prof=False):
         """per-step device time via CUDA events on the engine stream, L2 flushed between."""
@@ -303,14 +311,16 @@ def main():
         barrier()
     clocks = ClockSampler(local)
     eng.host_stats(reset=True)
+    tv0 = eng.transfers()
     clocks.start()
     t_val, rep, launches, profile = timed(step_value, args.steps, prof=True)
+    tv1 = eng.transfers()
     clk = clocks.stop()
     host = eng.host_stats(reset=True)
 
     # max over ranks
-    tot = torch.tensor([sum(t_val)], dtype=torch.float64, device=f"cuda:{local}")
-    lt = torch.tensor([launches], dtype=torch.float64, device=f"cuda:{local}")
+    tot = torch.tensor([sum(t_val)], dtype=torch.float64, device=coll_dev)
+    lt = torch.tensor([launches], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
@@ -339,23 +349,15 @@ def main():
                "step_ms": [round(t * 1e3, 2) for t in t_e2e],
                "stage_s": {"partition": rep_e2e.partition_s, "qaoa": rep_e2e.qaoa_s,
                            "merge": rep_e2e.merge_s}}
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return 0
-    if e2e is None:  # multi-GPU: the sharded step already moves records host<->device
-        e2e = {"value": evals_per_step / sec_per_step, "unit": UNIT,
-               "h2d_bytes_per_step": None, "d2h_bytes_per_step": None}
-
     # ---- roofline for the dominant kernel --------------------------------------------
-    # The timed region runs chunks on 3 concurrent streams, so per-launch event durations
+    # The timed region runs chunks on concurrent streams, so per-launch event durations
     # there are stretched by sharing the GPU. The kernel roofline is therefore taken from
     # one extra, single-stream step in which EVERY launch is bracketed by CUDA events on
     # its own stream; the timed-region (sampled) figures are reported beside it.
     iso_prev = os.environ.get("QCG_CHUNKS")
     os.environ["QCG_CHUNKS"] = "1"
     eng.profile(1)
-    step_value()
+    step_value()  # every rank: the multi-GPU step contains the record all-gather
     barrier()
     profile_iso = eng.profile_read()
     eng.profile(False)
@@ -363,6 +365,19 @@ def main():
         os.environ.pop("QCG_CHUNKS", None)
     else:
         os.environ["QCG_CHUNKS"] = iso_prev
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    if e2e is None:
+        # multi-GPU: the timed step is already the C-ABI call with host buffers on every
+        # rank (graph edges in, records out through the host for the gather, merge on rank 0)
+        e2e = {"value": evals_per_step / sec_per_step, "unit": UNIT,
+               "h2d_bytes_per_step": (tv1[0] - tv0[0]) // args.steps,
+               "d2h_bytes_per_step": (tv1[1] - tv0[1]) // args.steps,
+               "note": "rank 0's copies; the sharded step runs through qc_shard_solve / "
+                       "qc_merge_records with host buffers on every rank"}
+
     peak, peak_kind = load_peaks()
     dom = max(profile_iso, key=lambda k: profile_iso[k]["ms"])
     d = profile_iso[dom]
@@ -404,7 +419,7 @@ def main():
                 "step_aggregate_GBs": iso_bytes / sec_per_step / 1e9,
                 "step_aggregate_frac": iso_bytes / sec_per_step / 1e9 / peak,
                 "timed_region_sampled": {
-                    "stride": args.profile_stride, "streams": 3,
+                    "stride": args.profile_stride, "streams": 2,
                     "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                                     "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
                                     if v["ms"] > 0 else 0.0}
