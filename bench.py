@@ -202,7 +202,7 @@ def run_reference_arm(args, w):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": statistics.median(totals) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
                    "qubit_cap": w["qubit_cap"], "layers": w["layers"], "top_k": w["top_k"],
                    "budget": w["budget"], "parallelism": f"cpu x{cores} threads"},
