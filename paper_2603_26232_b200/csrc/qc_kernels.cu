@@ -562,9 +562,12 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // ---------------------------------------------------------------------------
 constexpr int kSumParts = 8;                        // 16-double parts per chunk
 constexpr int kSumChunk = 16 * kSumParts;           // doubles per chunk per chain (1 KB)
-constexpr int kSumStages = 3;
 constexpr size_t kSumStageBytes = 32 * kSumChunk * sizeof(double);  // 32 KB
-constexpr size_t kSumSmem = kSumStages * kSumStageBytes + 1024 + kSumStages * 8;
+// stages in flight: 3 lets two warp-CTAs share an SM (launches of more warps than SMs);
+// a launch that fits one warp per SM uses 6 (each 32 KB tensor copy takes ~1 us in the
+// SM's TMA unit, so deeper lookahead hides it)
+template <int STAGES>
+constexpr size_t sum_smem() { return STAGES * kSumStageBytes + 1024 + STAGES * 8; }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -574,6 +577,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // part (128 B stride)}, box {16, 32, kSumParts}, 128-byte swizzle: the shared box is
 // [part][block][16 doubles] and 16-byte unit u of row r sits at unit u ^ (r & 7), so the
 // 32 lanes (one block each) read one part conflict-free.
+template <int kSumStages>
 __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
                                                 int n_slots, int Q, int sym,
                                                 double* __restrict__ partials,
@@ -630,12 +634,11 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
                 : "memory");
         }
     };
-    issue(0);
-    issue(1);
+    for (int c = 0; c + 1 < kSumStages; ++c) issue(c);
     double acc = 0.0;
     const unsigned sw = static_cast<unsigned>(lane & 7);
     for (int c = 0; c < kChunks; ++c) {
-        issue(c + 2);
+        issue(c + kSumStages - 1);
         wait(c);
         const unsigned char* st = sbase + (c % kSumStages) * kSumStageBytes;
         if (!desc) {
@@ -899,16 +902,24 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int nbl = 1 << (Q - 12);
         const int bpw = std::min(32, nbl);
         const int warps = (nbl / bpw) * (plan.sym ? 2 : 1) * n_slots;
-        static bool sum_attr = false;
-        if (!sum_attr) {
-            QC_CUDA(cudaFuncSetAttribute(k_blocksum, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSumSmem)));
-            sum_attr = true;
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            QC_CUDA(cudaGetDevice(&dev));
+            QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<3>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<6>())));
         }
         const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
-        launch_ex(k_blocksum, dim3(warps), dim3(32), kSumSmem, stream, pdl_ok, tmap, n_slots, Q,
-                  plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+        if (warps <= sms)
+            launch_ex(k_blocksum<6>, dim3(warps), dim3(32), sum_smem<6>(), stream, pdl_ok, tmap,
+                      n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+        else
+            launch_ex(k_blocksum<3>, dim3(warps), dim3(32), sum_smem<3>(), stream, pdl_ok, tmap,
+                      n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());
