@@ -336,7 +336,7 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
                              reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
                              reinterpret_cast<double*>(fb),
-                             part, tick, od, cs, &stats, &prof);
+                             part, tick, od, cs, &stats, &prof, st);
     if (flags & F_EXPECT) {
         auto* ho = static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8));
         d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);

@@ -171,14 +171,17 @@ int launch_levels(const uint32_t* d_eu, const uint32_t* d_ev, const double* d_ew
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
                  int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
                  unsigned* d_tickets, double* d_out, cudaStream_t stream,
-                 const ChainStats* stats = nullptr, Prof* prof = nullptr);
+                 const ChainStats* stats = nullptr, Prof* prof = nullptr,
+                 const void* state_base = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
 // v4 streaming passes (qc_pass.cu): persistent, one CTA per SM. pdl: launched with
 // programmatic stream serialization (the kernel's prologue overlaps the previous kernel's
 // tail; it waits with griddepcontrol.wait before touching state memory). Only for a
 // kernel whose stream predecessor is a kernel of the same chain.
+// state_base: the stored state of d_slots[0] (slots contiguous), for the TMA variant
 int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
-                   int n_slots, cudaStream_t stream, bool pdl = false);
+                   int n_slots, cudaStream_t stream, bool pdl = false,
+                   const void* state_base = nullptr);
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
                    const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream,
                    bool pdl = false);

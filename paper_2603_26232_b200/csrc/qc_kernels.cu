@@ -787,7 +787,7 @@ size_t partials_per_slot(const ChainPlan& plan) {
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
                  int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
                  unsigned* d_tickets, double* d_out, cudaStream_t stream, const ChainStats* stats,
-                 Prof* prof) {
+                 Prof* prof, const void* state_base) {
     if (n_slots <= 0) return 0;
     const int Q = plan.Q;
     const double N = static_cast<double>(size_t{1} << Q);
@@ -861,7 +861,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         if (v3)
             k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         else
-            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & F_FP32), n_slots, stream, pdl_ok && l > 0);
+            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & F_FP32), n_slots, stream, pdl_ok && l > 0,
+                           state_base);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {

@@ -25,10 +25,13 @@
 // ascending order, the mirror op (RX on qubit q-1 in half-state storage) comes last, and
 // mixer_pair is bitwise symmetric in its two operands (IEEE add/mul commute), so the
 // order of a pair's roles is immaterial.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
+#include <string>
 #include <type_traits>
 
 #include "qc_amp.cuh"
@@ -40,7 +43,7 @@ namespace v4 {
 constexpr int kGT = 256;             // threads per consumer group
 constexpr int kThreads = 2 * kGT;    // two groups
 constexpr int kStages = 3;
-constexpr int kLutCap = 256;         // LUT entries kept per group in shared memory
+constexpr int kLutCap = 224;         // LUT entries kept per group in shared memory
 constexpr int kDescCap = 24;         // slot descriptors cached per CTA
 constexpr uint32_t kStageAmpBytes = 4096u * 16u;
 constexpr uint32_t kOffLev = kStages * kStageAmpBytes;             // levels per stage (8 KB)
@@ -61,7 +64,7 @@ struct PD {
     int32_t phase, mix, lut_len, key;
 };
 constexpr uint32_t kSmem = kOffDesc + kDescCap * sizeof(PD);
-static_assert(kSmem <= 232448, "shared memory budget");
+static_assert(kSmem + 1024 <= 232448, "shared memory budget (+1 KB alignment slack for TMA)");
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -289,6 +292,185 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[((j + 8) << 8) | gt] = a[j + 8];
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// pass A, TMA variant (fp64 default; QCG_PASS_A=v4 for the cp.async/STG kernel above): the
+// compute warps issue no global memory
+// instructions. One elected lane per group moves the data: a 3-D tensor copy brings the
+// 64 KB tile in ({16 doubles, 256 sixteen-amp groups (stride 256 B), 2 halves (stride
+// 128 B)}, 128-byte swizzle: row r = m + 256*half, so rounds R0/R1/R2 read conflict-free),
+// a 1-D bulk copy the levels; results are staged linearly in the same stage and leave by
+// one 64 KB bulk store, after which the lane refills the stage.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ph5(uint32_t e) {  // tile index -> 16-byte unit
+    const uint32_t m = e >> 4, half = (e >> 3) & 1u, u = e & 7u;
+    return ((m + (half << 8)) << 3) | (u ^ (m & 7u));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_a5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
+              int Q, uint32_t flags, uint32_t total_tiles, const __grid_constant__ CUtensorMap tmap) {
+    using V = double2;
+    using A = Amp<double2>;
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // TMA 128B swizzle
+    const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
+    const int tshift = Q - 12;
+    const uint32_t tmask = (1u << tshift) - 1u;
+    const bool init = flags & F_INIT;
+    uint32_t t0;
+    int cnt;
+    tile_range(total_tiles, t0, cnt);
+    if (cnt <= 0) return;
+    const uint32_t sa = t0 >> tshift;
+    PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
+    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    const uint32_t bar0 = su32(sm + kOffBar);
+    volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
+    if (tid < kStages) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + tid * 8u) : "memory");
+        tag[tid] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+
+    // elected lane of the calling group: fill stage k%3 with local tile k
+    auto issue = [&](int k) {
+        if (k >= cnt || gt != 0) return;
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const uint32_t base = (t & tmask) << 12;
+        const uint32_t bar = bar0 + s * 8u;
+        tag[s] = k;
+        const bool lv = d.phase && d.lev;
+        if (init || d.phase || d.mix) {
+            const uint32_t bytes = (init ? 0u : 65536u) + (lv ? 8192u : 0u);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                         : "memory");
+            if (!init)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                    "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(su32(sm + s * kStageAmpBytes)),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(t << 8), "r"(0), "r"(bar)
+                    : "memory");
+            if (lv)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 8192, [%2];\n" ::"r"(
+                        su32(sm + kOffLev + s * 8192u)),
+                    "l"(d.lev + base), "r"(bar)
+                    : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+        }
+    };
+    if (g == 0) {
+        issue(0);
+        issue(2);
+    } else {
+        issue(1);
+    }
+
+    V* slut = reinterpret_cast<V*>(sm + kOffLut) + g * kLutCap;
+    int lut_owner = -1;
+    int pending = -1;  // local tile whose refill waits on this group's last bulk store
+    for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool act = init || d.phase || d.mix;
+        const bool use_lev = d.phase && d.lev;
+        const bool lut_sm = use_lev && d.lut_len <= kLutCap;
+        if (lut_sm && lut_owner != d.key) {
+            const V* lsrc = reinterpret_cast<const V*>(d.lut);
+            for (int i = static_cast<int>(gt); i < d.lut_len; i += kGT) slut[i] = lsrc[i];
+            lut_owner = d.key;
+            grp_sync(g);
+        }
+        while (tag[s] != k) {
+        }
+        bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
+        if (pending >= 0) {
+            if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            issue(pending);
+            pending = -1;
+        }
+        if (!act) {
+            grp_sync(g);
+            issue(k + kStages);
+            continue;
+        }
+        const uint32_t base = (t & tmask) << 12;
+        V* st = reinterpret_cast<V*>(sm + s * kStageAmpBytes);
+        const double c = d.c, sn = d.s;
+        const bool mix = d.mix;
+        V a[16];
+        {
+            const uint4* lv = reinterpret_cast<const uint4*>(sm + kOffLev + s * 8192u) + gt * 2u;
+            const V* lutp = lut_sm ? slut : reinterpret_cast<const V*>(d.lut);
+            const double amp0 = d.amp0;
+            const bool phase = d.phase;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = h * 8 + jj;
+                    const uint32_t e = gt * 16u + j;
+                    V v = init ? A::mk(amp0, 0.0) : st[ph5(e)];
+                    if (phase) {
+                        if (use_lev) {
+                            const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
+                                                : (jj >> 1) == 2 ? l4.z : l4.w;
+                            v = A::cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
+                        } else {
+                            v = phase_frac<V>(v, d.gamma, d.val[base + e]);
+                        }
+                    }
+                    a[j] = v;
+                }
+            }
+            if (mix) rx_local<V, 0, 4>(a, c, sn);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[ph5(gt * 16u + j)] = a[j];
+        }
+        grp_sync(g);
+        {
+            const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = st[ph5(r | (j << 4))];
+            if (mix) rx_local<V, 0, 4>(a, c, sn);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[ph5(r | (j << 4))] = a[j];
+        }
+        grp_sync(g);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st[ph5((j << 8) | gt)];
+        grp_sync(g);  // the stage's tile is in registers: it becomes the output staging
+        if (mix) rx_local<V, 0, 4>(a, c, sn);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) st[(j << 8) | gt] = a[j];  // linear, conflict-free
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        grp_sync(g);
+        if (gt == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 65536;\n" ::"l"(
+                             d.state + base),
+                         "r"(su32(st))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        // the refill of this stage waits for the store to have read it: done by the elected
+        // lane after its next wait (the read is long finished by then), not stalling here
+        pending = k + kStages;
+    }
+    if (pending >= 0) {
+        if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        issue(pending);
+    }
+    if (gt == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -534,10 +716,66 @@ int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
 
 size_t pass4_smem() { return v4::kSmem; }
 
+namespace {
+using EncodeTiledFn5 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// the launch's contiguous stored states as {16 doubles, 16-amp groups, 2 halves}
+CUtensorMap state_tensor_map(const void* base, uint64_t amps) {
+    static EncodeTiledFn5 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        QC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) internal_error("cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<EncodeTiledFn5>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {16, amps / 16, 2};
+    const cuuint64_t strides[2] = {256, 128};
+    const cuuint32_t box[3] = {16, 256, 2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims,
+                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) internal_error("state tensor map: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+bool tma_pass_a() {  // default for fp64; QCG_PASS_A=v4 selects the cp.async/STG version
+    static const bool on = [] {
+        const char* e = std::getenv("QCG_PASS_A");
+        return !(e && std::string(e) == "v4");
+    }();
+    return on;
+}
+}  // namespace
+
 int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q, uint32_t flags,
-                   int n_slots, cudaStream_t stream, bool pdl) {
+                   int n_slots, cudaStream_t stream, bool pdl, const void* state_base) {
     const int sms = sm_count();
     const bool fp32 = flags & F_FP32;
+    if (tma_pass_a() && !fp32 && state_base) {
+        static bool attr = false;
+        if (!attr) {
+            QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(v4::kSmem + 1024)));
+            attr = true;
+        }
+        int launches = 0;
+        for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
+            const int n = std::min(n_slots - s0, slots_per_launch(sms));
+            const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
+            const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+            const CUtensorMap tm = state_tensor_map(
+                static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * 16,
+                static_cast<uint64_t>(n) << Q);
+            launch_ex(v4::k_pass_a5, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
+            ++launches;
+        }
+        return launches;
+    }
     int launches = 0;
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
