@@ -62,6 +62,7 @@ enum : uint32_t {
     F_STATE_OUT = 4u,   // final state must be written back
     F_SYM = 8u,         // half-state storage (complement symmetry), else full state
     F_FP32 = 64u,       // optional fp32 mode: float2 amplitudes, float f(z), fp32 LUTs (1e-4)
+    F_TSTORE = 128u,    // pass B (TMA): results leave by tensor stores (default)
 };
 
 // One high (gather) pass: 3 column bits (0,1,2) + kHighBits tile bits.
@@ -184,7 +185,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
                    const void* state_base = nullptr);
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
                    const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream,
-                   bool pdl = false);
+                   bool pdl = false, const void* state_base = nullptr);
 
 // cudaLaunchKernelEx with the programmatic-stream-serialization attribute
 template <typename... KArgs, typename... Args>

@@ -884,7 +884,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                 k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
                     d_slots, d_lp, l, Q, plan.high[h], fh);
             else
-                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & F_FP32), n_slots, stream, pdl_ok);
+                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & F_FP32), n_slots, stream, pdl_ok,
+                               state_base);
             if (prof) prof->end(stream);
             ++launches;
         }

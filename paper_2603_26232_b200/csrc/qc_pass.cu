@@ -687,6 +687,275 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// pass B, TMA variant (fp64, Q >= 21 by default; QCG_PASS_B=v4|tma forces a kernel).
+// The 9 gather bits of a HighPass are [NT RX targets (one contiguous run of stored bits)]
+// [mirror, if HM] [pads: bits 3.. (contiguous)], so a tile is one box of a 5-D tensor view
+// of the launch's states: {16 doubles (column bits 0-2), targets, pads, low free run, high
+// free run x slots}; the mirror partners (x -> ~x) are a second 32 KB box at the
+// complemented free coordinates, whose elements sit in the box in reversed order. Box row
+// r = targets | pads << NT (128 bytes, 128-byte swizzle: unit u at u ^ (r & 7)). Under the
+// complement both the row and the column reverse, so the swizzled unit is unchanged:
+//   byte(e) = m << 15 | (r0 ^ (m ? 255 : 0)) << 7 | ((w ^ r0) & 7) << 4.
+// Compute rounds are v4's; results go back to the same box positions and leave by tensor
+// stores of the same boxes (F_TSTORE), or straight from registers. Levels (f passes) still
+// arrive by per-thread cp.async, so a stage's barrier then expects 256 + 1 arrivals.
+// ---------------------------------------------------------------------------
+struct B5Geo {
+    uint32_t lo_shift, lo_mask;   // low free run of stored bits (incl. a pinned mirror bit)
+    uint32_t hi_shift, hi_mask;   // high free run (merged with the slot index)
+    uint32_t hi_bits, allq;       // allq: the Q stored-bit mask (mirror complement)
+};
+
+template <int NT, int HM>
+__device__ __forceinline__ uint32_t pb5(uint32_t e) {
+    const uint32_t w = e & 7u, gb = e >> 3;
+    if constexpr (HM == 0) {
+        return (gb << 7) | (((w ^ gb) & 7u) << 4);
+    } else {
+        constexpr uint32_t L = (1u << NT) - 1u;
+        const uint32_t m = (gb >> NT) & 1u;
+        const uint32_t r0 = ((gb & L) | ((gb >> 1) & ~L)) & 255u;
+        return (m << 15) | ((r0 ^ (0u - m)) & 255u) << 7 | (((w ^ r0) & 7u) << 4);
+    }
+}
+
+template <int NT, int HM>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_b5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
+              int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles,
+              const __grid_constant__ B5Geo geo, const __grid_constant__ CUtensorMap tmap) {
+    using V = double2;
+    using A = Amp<double2>;
+    using S = double;
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // 128B swizzle
+    const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
+    const int tshift = Q - 12;
+    const uint32_t tmask = (1u << tshift) - 1u;
+    const bool fout = flags & F_EXPECT;
+    const bool sout = !fout || (flags & F_STATE_OUT);
+    const bool tstore = flags & F_TSTORE;  // results leave by tensor stores of the boxes
+    uint32_t t0;
+    int cnt;
+    tile_range(total_tiles, t0, cnt);
+    if (cnt <= 0) return;
+    const uint32_t sa = t0 >> tshift;
+    PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
+    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    const uint32_t bar0 = su32(sm + kOffBar);
+    volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
+    volatile uint32_t* sxb = reinterpret_cast<volatile uint32_t*>(sm + kOffTag + 16);
+    if (tid < kStages) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar0 + tid * 8u),
+                     "r"(fout ? kGT + 1 : 1)
+                     : "memory");
+        tag[tid] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+    const int nr = (hp.kind[8] != 0) ? 3 : ((hp.kind[4] != 0) ? 2 : 1);
+    const uint32_t w = gt & 7u;
+    const uint32_t tx_lev = hx(hp, gt & 255u);
+
+    auto tma = [&](bool store, uint32_t sdst, uint32_t x, uint32_t slot, uint32_t bar) {
+        const int c3 = static_cast<int>((x >> geo.lo_shift) & geo.lo_mask);
+        const int c4 = static_cast<int>(((x >> geo.hi_shift) & geo.hi_mask) | (slot << geo.hi_bits));
+        if (store)
+            asm volatile(
+                "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmap)),
+                "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(sdst)
+                : "memory");
+        else
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(sdst),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(0), "r"(0), "r"(c3), "r"(c4), "r"(bar)
+                : "memory");
+    };
+    // whole group: fill stage k%3 with local tile k (box loads by the elected lane, levels
+    // by every thread on f passes)
+    auto issue = [&](int k) {
+        if (k >= cnt) return;
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const uint32_t bar = bar0 + s * 8u;
+        const bool act = d.mix || fout;
+        const bool lead = gt == 0;
+        if (!lead && !fout) return;
+        const uint32_t xb = deposit4(t & tmask, hp.freemask);
+        if (lead) {
+            sxb[s] = xb;
+            tag[s] = k;
+            if (act) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(65536u)
+                             : "memory");
+                const uint32_t sdst = su32(sm + s * kStageAmpBytes);
+                tma(false, sdst, xb, t >> tshift, bar);
+                if (HM) tma(false, sdst + 32768u, xb ^ geo.allq, t >> tshift, bar);
+            } else {
+                bar_arrive(bar);
+            }
+        }
+        if (fout) {
+            if (d.lev) {
+                const uint32_t lb = su32(sm + kOffLev + s * 8192u);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const uint32_t gx = (xb ^ tx_lev ^ (i ? hp.mask[8] : 0u)) & ~7u;
+                    cpa16(lb + (gt + kGT * i) * 16u, d.lev + gx);
+                }
+                cpa_arrive(bar);
+            } else {
+                bar_arrive(bar);
+            }
+        }
+    };
+    if (g == 0) {
+        issue(0);
+        issue(2);
+    } else {
+        issue(1);
+    }
+
+    int pending = -1;  // local tile whose refill waits on this group's last tensor store
+    for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        const int s = k % kStages;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool mix = d.mix;
+        while (tag[s] != k) {
+        }
+        bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
+        if (pending >= 0) {
+            if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            issue(pending);
+            pending = -1;
+        }
+        if (!mix && !fout) {
+            grp_sync(g);
+            issue(k + kStages);
+            continue;
+        }
+        const int nrr = mix ? nr : 1;
+        const uint32_t xs = sxb[s];
+        const uint32_t xb = xs | w;
+        const S c = d.c, sn = d.s;
+        unsigned char* stb = sm + s * kStageAmpBytes;
+        const uint16_t* slev = reinterpret_cast<const uint16_t*>(sm + kOffLev + s * 8192u);
+        S* const gf = d.fbuf;
+        const uint16_t* const glev = d.lev;
+        const double* const gval = d.val;
+        V a[16];
+        auto at = [&](uint32_t e) -> V& { return *reinterpret_cast<V*>(stb + pb5<NT, HM>(e)); };
+        auto e_of = [&](auto R, int j) -> uint32_t {
+            if constexpr (decltype(R)::value == 0)
+                return w | (static_cast<uint32_t>(j) << 3) | ((gt >> 3) << 7);
+            else if constexpr (decltype(R)::value == 1)
+                return w | (((gt >> 3) & 15u) << 3) | (static_cast<uint32_t>(j) << 7) | ((gt >> 7) << 11);
+            else
+                return w | ((static_cast<uint32_t>(j >> 1) & 7u) << 3) | ((gt >> 3) << 6) |
+                       (static_cast<uint32_t>(j & 1) << 11);
+        };
+        auto finish = [&](auto R) {
+            constexpr int r = decltype(R)::value;
+            const uint32_t txt = r == 0 ? hx(hp, (gt >> 3) << 4)
+                               : r == 1 ? hx(hp, ((gt >> 3) & 15u) | ((gt >> 7) << 8))
+                                        : hx(hp, (gt >> 3) << 3);
+            const uint32_t xt = xb ^ txt;
+            if (!tstore) {  // registers -> global; the stage refills once every thread read it
+                if (!fout) {
+                    grp_sync(g);
+                    issue(k + kStages);
+                }
+                V* const gstate = reinterpret_cast<V*>(d.state);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t gidx = xt ^ hx(hp, gb_local<r>(j));
+                    if (sout) __stcs(gstate + gidx, a[j]);
+                    if (fout) {
+                        S cst;
+                        if (glev)
+                            cst = static_cast<S>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
+                        else
+                            cst = gval ? gval[gidx] : 1.0;
+                        gf[gidx] = A::mul(A::nrm(a[j]), cst);
+                    }
+                }
+                if (fout) {
+                    grp_sync(g);  // levels of the stage read
+                    issue(k + kStages);
+                }
+                return;
+            }
+            if (fout) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t gidx = xt ^ hx(hp, gb_local<r>(j));
+                    S cst;
+                    if (glev)
+                        cst = static_cast<S>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
+                    else
+                        cst = gval ? gval[gidx] : 1.0;
+                    gf[gidx] = A::mul(A::nrm(a[j]), cst);  // stays in L2 for k_blocksum
+                }
+            }
+            if (sout) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) at(e_of(R, j)) = a[j];
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                grp_sync(g);
+                if (gt == 0) {
+                    const uint32_t sb = su32(stb);
+                    tma(true, sb, xs, t >> tshift, 0);
+                    if (HM) tma(true, sb + 32768u, xs ^ geo.allq, t >> tshift, 0);
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+                pending = k + kStages;
+            } else {
+                grp_sync(g);  // levels of the stage read
+                issue(k + kStages);
+            }
+        };
+        using R0 = std::integral_constant<int, 0>;
+        using R1 = std::integral_constant<int, 1>;
+        using R2 = std::integral_constant<int, 2>;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = at(e_of(R0{}, j));
+        if (mix) ops_local<V, 0, 4>(a, hp, c, sn);
+        if (nrr == 1) {
+            finish(R0{});
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) at(e_of(R0{}, j)) = a[j];
+        grp_sync(g);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = at(e_of(R1{}, j));
+        ops_local<V, 4, 4>(a, hp, c, sn);
+        if (nrr == 2) {
+            finish(R1{});
+            continue;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) at(e_of(R1{}, j)) = a[j];
+        grp_sync(g);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = at(e_of(R2{}, j));
+        ops_local<V, 8, 1>(a, hp, c, sn);
+        finish(R2{});
+    }
+    if (pending >= 0) {
+        if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        issue(pending);
+    }
+    if (gt == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
 }  // namespace v4
 
 
@@ -722,7 +991,7 @@ using EncodeTiledFn5 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 // the launch's contiguous stored states as {16 doubles, 16-amp groups, 2 halves}
-CUtensorMap state_tensor_map(const void* base, uint64_t amps) {
+EncodeTiledFn5 tensor_encoder() {
     static EncodeTiledFn5 encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -731,6 +1000,10 @@ CUtensorMap state_tensor_map(const void* base, uint64_t amps) {
         if (!fn || q != cudaDriverEntryPointSuccess) internal_error("cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<EncodeTiledFn5>(fn);
     }
+    return encode;
+}
+CUtensorMap state_tensor_map(const void* base, uint64_t amps) {
+    const EncodeTiledFn5 encode = tensor_encoder();
     CUtensorMap m;
     const cuuint64_t dims[3] = {16, amps / 16, 2};
     const cuuint64_t strides[2] = {256, 128};
@@ -792,11 +1065,154 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     return launches;
 }
 
+namespace {
+using B5Kernel = void (*)(const SlotDesc*, const LayerParam*, int, int, HighPass, uint32_t, uint32_t,
+                          v4::B5Geo, CUtensorMap);
+template <int NT, int HM>
+B5Kernel b5_kernel() {
+    static bool attr = false;
+    if (!attr) {
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b5<NT, HM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kSmem + 1024)));
+        attr = true;
+    }
+    return v4::k_pass_b5<NT, HM>;
+}
+B5Kernel b5_lookup(int nt, int hm) {
+    switch (nt * 2 + hm) {
+        case 1: return b5_kernel<0, 1>();
+        case 2: return b5_kernel<1, 0>();
+        case 3: return b5_kernel<1, 1>();
+        case 4: return b5_kernel<2, 0>();
+        case 5: return b5_kernel<2, 1>();
+        case 6: return b5_kernel<3, 0>();
+        case 7: return b5_kernel<3, 1>();
+        case 8: return b5_kernel<4, 0>();
+        case 9: return b5_kernel<4, 1>();
+        case 10: return b5_kernel<5, 0>();
+        case 11: return b5_kernel<5, 1>();
+        case 12: return b5_kernel<6, 0>();
+        case 13: return b5_kernel<6, 1>();
+        case 14: return b5_kernel<7, 0>();
+        case 15: return b5_kernel<7, 1>();
+        case 16: return b5_kernel<8, 0>();
+        case 17: return b5_kernel<8, 1>();
+        case 18: return b5_kernel<9, 0>();
+        default: return nullptr;
+    }
+}
+
+// HighPass -> 5-D box geometry of k_pass_b5 over a launch's contiguous states. False if
+// the pass lacks the [targets][mirror][pads] run structure (then v4 runs it).
+struct B5Plan {
+    int nt = 0, hm = 0;
+    v4::B5Geo geo{};
+    cuuint64_t dims[5];
+    cuuint64_t strides[4];
+    cuuint32_t box[5];
+};
+bool b5_plan(const HighPass& hp, int Q, B5Plan& P) {
+    int nt = 0, npad = 0, tstart = -1;
+    uint32_t tmask = 0, pmask = 0;
+    for (int b = 0; b < kHighBits; ++b) {
+        if (hp.kind[b] == 1) {
+            if (npad || P.hm) return false;  // targets come first
+            const int bit = __builtin_ctz(hp.mask[b]);
+            if (tstart < 0) tstart = bit;
+            if (bit != tstart + nt) return false;  // one contiguous run
+            tmask |= hp.mask[b];
+            ++nt;
+        } else if (hp.kind[b] == 2) {
+            if (npad || b != nt) return false;
+            P.hm = 1;
+        } else {
+            if (hp.mask[b] != (1u << (3 + npad))) return false;  // pads: bits 3, 4, ...
+            pmask |= hp.mask[b];
+            ++npad;
+        }
+    }
+    P.nt = nt;
+    const uint32_t allq = (Q == 32) ? ~0u : ((1u << Q) - 1u);
+    const uint32_t fr = allq & ~(7u | tmask | pmask);  // free bits incl. a pinned mirror bit
+    if (!fr) return false;
+    const int lo = __builtin_ctz(fr);
+    int lo_bits = 0;
+    while (lo + lo_bits < Q && ((fr >> (lo + lo_bits)) & 1u)) ++lo_bits;
+    const uint32_t rest = fr & ~(((1u << lo_bits) - 1u) << lo);
+    int hi = Q, hi_bits = 0;
+    if (rest) {
+        hi = __builtin_ctz(rest);
+        hi_bits = Q - hi;
+        if ((rest >> hi) != (1u << hi_bits) - 1u) return false;  // must run up to Q-1
+    }
+    if (P.hm && hi_bits) return false;  // a mirror pass ends at the top stored bit
+    P.geo = v4::B5Geo{static_cast<uint32_t>(lo), (1u << lo_bits) - 1u, static_cast<uint32_t>(hi),
+                      (1u << hi_bits) - 1u, static_cast<uint32_t>(hi_bits), allq};
+    // dims: 0 columns, 1 targets (or their low 8), 2 pads (or the 9th target, or size 1),
+    // 3 low free run, 4 high free run x slots (size set per launch)
+    P.dims[0] = P.box[0] = 16;
+    P.dims[1] = P.box[1] = 1u << std::min(nt, 8);
+    P.strides[0] = nt ? (16ull << tstart) : 16ull;
+    if (nt == 9) {
+        P.dims[2] = P.box[2] = 2;
+        P.strides[1] = 16ull << (tstart + 8);
+    } else {
+        P.dims[2] = P.box[2] = 1u << npad;
+        P.strides[1] = 128;
+    }
+    P.dims[3] = 1ull << lo_bits;
+    P.box[3] = 1;
+    P.strides[2] = 16ull << lo;
+    P.box[4] = 1;
+    P.strides[3] = 16ull << hi;
+    return (nt + P.hm + npad) == kHighBits && b5_lookup(nt, P.hm) != nullptr;
+}
+// fp64 pass B kernel: the TMA kernel (tensor stores) where it measured faster, Q >= 21
+// (q=24: -3.5%, q=26: -4.1% per launch); at Q <= 19 v4's per-thread gathers are as fast
+// or faster (profiles/r1_pass_b_tma.txt). QCG_PASS_B=v4|tma forces one.
+bool tma_pass_b(int Q) {
+    static const int mode = [] {
+        const char* e = std::getenv("QCG_PASS_B");
+        if (e && std::string(e) == "v4") return 0;
+        if (e && std::string(e) == "tma") return 1;
+        return 2;
+    }();
+    return mode == 1 || (mode == 2 && Q >= 21);
+}
+}  // namespace
+
 int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, int Q,
-                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream, bool pdl) {
+                   const HighPass& hp, uint32_t flags, int n_slots, cudaStream_t stream, bool pdl,
+                   const void* state_base) {
     const int sms = sm_count();
     const bool fp32 = flags & F_FP32;
     int launches = 0;
+    B5Plan P;
+    if (tma_pass_b(Q) && !fp32 && state_base && b5_plan(hp, Q, P)) {
+        static const bool tstore = [] {  // QCG_B5_STORE=stg: results leave from registers
+            const char* e = std::getenv("QCG_B5_STORE");
+            return !(e && std::string(e) == "stg");
+        }();
+        const B5Kernel kern = b5_lookup(P.nt, P.hm);
+        for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
+            const int n = std::min(n_slots - s0, slots_per_launch(sms));
+            const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
+            const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+            P.dims[4] = (1ull << P.geo.hi_bits) * static_cast<cuuint64_t>(n);
+            CUtensorMap tm;
+            const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+            const CUresult r = tensor_encoder()(
+                &tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+                const_cast<char*>(static_cast<const char*>(state_base)) + (static_cast<size_t>(s0) << Q) * 16,
+                P.dims, P.strides, P.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) internal_error("pass B tensor map: " + std::to_string(static_cast<int>(r)));
+            launch_ex(kern, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream, pdl || s0 > 0,
+                      d_slots + s0, d_lp, layer, Q, hp, flags | (tstore ? F_TSTORE : 0u), tiles, P.geo, tm);
+            ++launches;
+        }
+        return launches;
+    }
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);

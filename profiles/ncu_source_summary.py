@@ -7,10 +7,17 @@ import collections
 import csv
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
+rows = list(csv.reader(open(sys.argv[1], errors="replace")))
 hdr = rows[1]
-data = rows[2:]
 iS = hdr.index("Warp Stall Sampling (All Samples)")
+# the source page may list the SASS more than once: keep the first row per address
+ia = hdr.index("Address")
+seen = set()
+data = []
+for r in rows[2:]:
+    if len(r) > iS and r[iS].strip().isdigit() and r[ia] not in seen:
+        seen.add(r[ia])
+        data.append(r)
 src = hdr.index("Source")
 stall = [(i, h) for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 tot = sum(int(r[iS] or 0) for r in data)

@@ -1,0 +1,41 @@
+"""Helper for test_gpu_statevector.py::test_pass_b_kernel_variants (run in a subprocess so
+the QCG_PASS_B / QCG_B5_STORE kernel selection, read once per process, can be forced).
+
+Checks the engine against the oracle, bit-exact, at subgraph sizes covering every pass B
+geometry class: mirror passes with 1..8 targets (q = 14..21) and the 9-target pass
+followed by a mirror-only pass (q = 22); states (F_STATE_OUT) and expectations alone
+(eval_batch: the f pass without the state write). Prints OK.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.refpy import OracleLib  # noqa: E402
+from paper_2603_26232_b200 import Engine  # noqa: E402
+
+
+def main():
+    orc = OracleLib()
+    orc.set_qubit_cap(26)
+    eng = Engine(0)
+    threads = max(1, min(32, os.cpu_count() or 1))
+    for q in (14, 16, 19, 20, 21, 22):
+        e = orc.generate_er(q, 0.2, 100 + q)
+        rng = np.random.default_rng(q)
+        g = rng.uniform(0.1, 3.0, 2)
+        b = rng.uniform(0.1, 3.0, 2)
+        a0, x0 = orc.run_ansatz(q, e, g, b, threads=threads)
+        a1, x1 = eng.run_ansatz(q, e, g, b)
+        assert np.array_equal(a1, a0), f"q={q}: amplitudes differ"
+        assert x1 == x0, f"q={q}: expectation {x1!r} != {x0!r}"
+        got = eng.eval_batch([(q, e)], 2, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
+        assert got[0] == x0, f"q={q}: eval_batch {got[0]!r} != {x0!r}"
+    print("OK")
+
+
+if __name__ == "__main__":
+    main()

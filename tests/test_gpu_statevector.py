@@ -173,3 +173,19 @@ def test_identity_layers_in_multipass_chains(engine, oracle, q):
         a0, x0 = oracle.run_ansatz(q, e, g, b)
         a1, x1 = engine.run_ansatz(q, e, g, b)
         assert np.array_equal(a1, a0) and x1 == x0
+
+
+@pytest.mark.parametrize("env", [{"QCG_PASS_B": "tma"},
+                                 {"QCG_PASS_B": "tma", "QCG_B5_STORE": "stg"},
+                                 {"QCG_PASS_B": "v4"}],
+                         ids=["tma-tensor-store", "tma-register-store", "v4"])
+def test_pass_b_kernel_variants(env):
+    """Every pass B kernel (qc_pass.cu: TMA boxes with tensor or register stores, v4
+    per-thread gathers) bit-exact at all geometry classes (tests/gpu_pass_variants.py)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "gpu_pass_variants.py")],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-2000:]
