@@ -560,14 +560,14 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* _
 // stages) into its own shared-memory row. Partials land in full-index block order; the last warp of a slot (atomic
 // ticket) sums them in block order from 0.0 and writes the expectation.
 // ---------------------------------------------------------------------------
-constexpr int kSumParts = 8;                        // 16-double parts per chunk
-constexpr int kSumChunk = 16 * kSumParts;           // doubles per chunk per chain (1 KB)
-constexpr size_t kSumStageBytes = 32 * kSumChunk * sizeof(double);  // 32 KB
+// a stage holds kParts 16-double parts (128 B each) of each lane's chain: 4 KB per part
+template <int kParts>
+__host__ __device__ constexpr size_t sum_stage_bytes() { return size_t{32} * 16 * kParts * sizeof(double); }
 // stages in flight: 3 lets two warp-CTAs share an SM (launches of more warps than SMs);
 // a launch that fits one warp per SM uses 6 (each 32 KB tensor copy takes ~1 us in the
 // SM's TMA unit, so deeper lookahead hides it)
-template <int STAGES>
-constexpr size_t sum_smem() { return STAGES * kSumStageBytes + 1024 + STAGES * 8; }
+template <int STAGES, int PARTS>
+constexpr size_t sum_smem() { return STAGES * sum_stage_bytes<PARTS>() + 1024 + STAGES * 8; }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -577,12 +577,14 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // part (128 B stride)}, box {16, 32, kSumParts}, 128-byte swizzle: the shared box is
 // [part][block][16 doubles] and 16-byte unit u of row r sits at unit u ^ (r & 7), so the
 // 32 lanes (one block each) read one part conflict-free.
-template <int kSumStages>
+template <int kSumStages, int kSumParts>
 __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
                                                 int n_slots, int Q, int sym,
                                                 double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
+    constexpr int kSumChunk = 16 * kSumParts;  // doubles per chunk per chain
+    constexpr size_t kSumStageBytes = sum_stage_bytes<kSumParts>();
     extern __shared__ unsigned char sraw[];
     // 1024-byte aligned base by pointer arithmetic, so the compiler keeps the shared
     // address space (LDS instead of generic LD on the chain's operand path)
@@ -608,18 +610,19 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncwarp();
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // f is written by the previous pass
+    // lane 0 issues, by predication rather than a branch, so the (uniform) issue code can
+    // be scheduled into the gaps of the dependent add chain
     auto issue = [&](int c) {
-        if (c >= kChunks || lane != 0) return;
+        if (c >= kChunks) return;
         const int st = c % kSumStages;
         const int part0 = (desc ? kChunks - 1 - c : c) * kSumParts;
-        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar + st)),
-                     "r"(static_cast<unsigned>(kSumStageBytes))
-                     : "memory");
         asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(sbase + st * kSumStageBytes)),
-            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(gb0), "r"(part0),
-            "r"(smem_u32(mbar + st))
+            "{\n .reg .pred p;\n setp.eq.u32 p, %6, 0;\n"
+            " @p mbarrier.arrive.expect_tx.shared.b64 _, [%5], %7;\n"
+            " @p cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n}\n" ::"r"(smem_u32(sbase + st * kSumStageBytes)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(gb0), "r"(part0), "r"(smem_u32(mbar + st)),
+            "r"(lane), "r"(static_cast<unsigned>(kSumStageBytes))
             : "memory");
     };
     auto wait = [&](int c) {
@@ -705,7 +708,7 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-static CUtensorMap fbuf_tensor_map(double* fbuf, uint64_t total_blocks) {
+static CUtensorMap fbuf_tensor_map(double* fbuf, uint64_t total_blocks, int parts) {
     static EncodeTiledFn encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -717,7 +720,7 @@ static CUtensorMap fbuf_tensor_map(double* fbuf, uint64_t total_blocks) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {16, total_blocks, kBlock / 16};
     const cuuint64_t strides[2] = {kBlock * sizeof(double), 16 * sizeof(double)};
-    const cuuint32_t box[3] = {16, 32, kSumParts};
+    const cuuint32_t box[3] = {16, 32, static_cast<cuuint32_t>(parts)};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, fbuf, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -909,19 +912,22 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             int dev = 0;
             QC_CUDA(cudaGetDevice(&dev));
             QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sum_smem<3>())));
-            QC_CUDA(cudaFuncSetAttribute(k_blocksum<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sum_smem<6>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<3, 8>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<6, 8>())));
         }
-        const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl);
+        // stages x 1 KB-per-lane chunks: 6 deep when every warp has an SM to itself, else
+        // 3 (two warp-CTAs per SM). Smaller stages measured slower at every size
+        // (profiles/r1_blocksum_stages.txt).
+        const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl, 8);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
         if (warps <= sms)
-            launch_ex(k_blocksum<6>, dim3(warps), dim3(32), sum_smem<6>(), stream, pdl_ok, tmap,
-                      n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+            launch_ex(k_blocksum<6, 8>, dim3(warps), dim3(32), sum_smem<6, 8>(), stream, pdl_ok, tmap, n_slots,
+                      Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         else
-            launch_ex(k_blocksum<3>, dim3(warps), dim3(32), sum_smem<3>(), stream, pdl_ok, tmap,
-                      n_slots, Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+            launch_ex(k_blocksum<3, 8>, dim3(warps), dim3(32), sum_smem<3, 8>(), stream, pdl_ok, tmap, n_slots,
+                      Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());

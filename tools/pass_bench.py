@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--p-edge", type=float, default=0.1)
+    ap.add_argument("--per-launch", action="store_true",
+                    help="also report pass_low us per rep (spread of a sporadic slow run)")
     a = ap.parse_args()
     eng = Engine(0)
     graphs = [(a.q, generate_er(a.q, max(a.p_edge, 0.2), 100 + i)) for i in range(a.slots)]
@@ -32,6 +34,13 @@ def main():
     idx = np.arange(a.slots, dtype=np.int32)
     prm = rng.uniform(0.1, 3.0, size=(a.slots, 2 * a.layers))
     ref = eng.eval_batch(graphs, a.layers, idx, prm)  # warm-up (+ first-touch)
+    per = []
+    if a.per_launch:
+        for _ in range(a.reps):
+            eng.profile(True)
+            eng.eval_batch(graphs, a.layers, idx, prm)
+            v = eng.profile_read()["pass_low"]
+            per.append(round(1e3 * v["ms"] / max(v["launches"], 1), 1))
     eng.profile(True)
     for _ in range(a.reps):
         out = eng.eval_batch(graphs, a.layers, idx, prm)
@@ -44,7 +53,8 @@ def main():
             res[k] = dict(launches=v["launches"], us=round(us, 2),
                           GBs=round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1))
     print(json.dumps(dict(q=a.q, slots=a.slots, layers=a.layers,
-                          impl=os.environ.get("QCG_PASS", "4"), kernels=res)))
+                          impl=os.environ.get("QCG_PASS", "4"), kernels=res,
+                          pass_low_launch_us=per or None)))
 
 
 if __name__ == "__main__":
