@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[sw<V>(gt * 16u + j)] = a[j];
         }
-        grp_sync(g);
+        // round 1 reads only what its own half-warp wrote in round 0 (e>>8 = gt>>4)
+        __syncwarp();
         // round 1: bits 4-7, e = (gt>>4)<<8 | j<<4 | gt&15
         {
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[ph5(gt * 16u + j)] = a[j];
         }
-        grp_sync(g);
+        __syncwarp();  // round 1 reads only what its own half-warp wrote (e>>8 = gt>>4)
         {
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
 #pragma unroll
