@@ -274,8 +274,17 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
         ~size_t{255};
     const size_t lut_entry = fp32 ? 8 : 16;  // double2 (exact) or float2 LUT entries
     const size_t bytes = o_lut + lut_total * lut_entry;
-    char* h = static_cast<char*>(ctx.hstage.get(bytes));
-    char* d = static_cast<char*>(ctx.dstage.get(bytes));
+    // a replayed graph copies a fixed-size staging block: sized for every slot phasing
+    // every layer with the longest LUT of the solve, so it does not change step to step
+    const bool graph = use_graphs() && !prof.on;
+    size_t copy_bytes = bytes;
+    if (graph) {
+        size_t maxl = 0;
+        for (const DevGraph& x : dg) maxl = std::max(maxl, static_cast<size_t>(x.lut_len));
+        copy_bytes = o_lut + static_cast<size_t>(n) * static_cast<size_t>(std::max(p, 1)) * maxl * lut_entry;
+    }
+    char* h = static_cast<char*>(ctx.hstage.get(copy_bytes));
+    char* d = static_cast<char*>(ctx.dstage.get(copy_bytes));
     auto* hs = reinterpret_cast<SlotDesc*>(h);
     auto* hl = reinterpret_cast<LayerParam*>(h + o_lp);
     auto* hlut = reinterpret_cast<double*>(h + o_lut);
@@ -332,14 +341,49 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             }
         }
     }
-    h2d_copy(d, h, bytes, cs);
-    launches += launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
-                             reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
-                             reinterpret_cast<double*>(fb),
-                             part, tick, od, cs, &stats, &prof, st);
-    if (flags & F_EXPECT) {
-        auto* ho = static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8));
-        d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
+    double* ho = (flags & F_EXPECT) ? static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8)) : nullptr;
+    auto record = [&](size_t nbytes) {
+        h2d_copy(d, h, nbytes, cs);
+        const int k = launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
+                                   reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
+                                   reinterpret_cast<double*>(fb), part, tick, od, cs, &stats,
+                                   graph ? nullptr : &prof, st);
+        if (ho) d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
+        return k;
+    };
+    if (!graph) {
+        launches += record(bytes);
+    } else {
+        ChainKey key;
+        key.Q = plan.Q;
+        key.n = n;
+        key.p = p;
+        key.sym = plan.sym;
+        key.flags = flags;
+        const void* ptrs[8] = {st, fb, part, tick, od, d, h, ho};
+        for (int i = 0; i < 8; ++i) key.ptr[i] = ptrs[i];
+        key.copy_bytes = copy_bytes;
+        if (!ctx.gexec || !(ctx.gkey == key)) {
+            if (ctx.gexec) {
+                QC_CUDA(cudaGraphExecDestroy(ctx.gexec));
+                ctx.gexec = nullptr;
+            }
+            const uint64_t h0 = h2d, d0 = d2h;
+            cudaGraph_t g = nullptr;
+            QC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            ctx.glaunches = record(copy_bytes);
+            QC_CUDA(cudaStreamEndCapture(cs, &g));
+            QC_CUDA(cudaGraphInstantiate(&ctx.gexec, g, 0));
+            QC_CUDA(cudaGraphDestroy(g));
+            h2d = h0;  // counted per replay below
+            d2h = d0;
+            ctx.gkey = key;
+            ++graph_captures;
+        }
+        QC_CUDA(cudaGraphLaunch(ctx.gexec, cs));
+        launches += ctx.glaunches;
+        h2d += copy_bytes;
+        if (ho) d2h += static_cast<uint64_t>(n) * 8;
     }
     if (!ctx.done) QC_CUDA(cudaEventCreateWithFlags(&ctx.done, cudaEventDisableTiming));
     QC_CUDA(cudaEventRecord(ctx.done, cs));

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -57,6 +59,23 @@ struct EvalPoint {
 };
 
 // Staging + completion event of one in-flight launch chain ("chunk" of slots).
+// Identity of a captured chain: everything the recorded nodes depend on (shape, flags and
+// every buffer address baked into kernel arguments or copy nodes).
+struct ChainKey {
+    int Q = -1, n = 0, p = 0;
+    bool sym = false;
+    uint32_t flags = 0;
+    const void* ptr[8] = {};  // states, f, partials, tickets, out, device/host staging, host out
+    size_t copy_bytes = 0;
+    bool operator==(const ChainKey& o) const {
+        if (Q != o.Q || n != o.n || p != o.p || sym != o.sym || flags != o.flags || copy_bytes != o.copy_bytes)
+            return false;
+        for (int i = 0; i < 8; ++i)
+            if (ptr[i] != o.ptr[i]) return false;
+        return true;
+    }
+};
+
 struct ChunkCtx {
     DevBuf dstage;
     HostBuf hstage, hout;
@@ -65,10 +84,16 @@ struct ChunkCtx {
     uint32_t flags = 0;
     double* d_out = nullptr;
     cudaStream_t st = nullptr;  // stream the chunk runs on (null: the engine stream)
+    // CUDA graph of this chunk's step (staging upload -> launch chain -> result read),
+    // captured once per ChainKey and replayed each lockstep step
+    cudaGraphExec_t gexec = nullptr;
+    ChainKey gkey;
+    int glaunches = 0;
     ChunkCtx() = default;
     ChunkCtx(const ChunkCtx&) = delete;
     ChunkCtx& operator=(const ChunkCtx&) = delete;
     ~ChunkCtx() {
+        if (gexec) cudaGraphExecDestroy(gexec);
         if (done) cudaEventDestroy(done);
     }
 };
@@ -88,6 +113,15 @@ struct qc_engine {
     qcg::DeviceArena merge_arena;                           // merge scratch, reused
     std::vector<std::unique_ptr<qcg::ChunkCtx>> chunk_pool;  // per-chunk staging, reused
     uint64_t h2d = 0, d2h = 0;  // bytes copied host<->device by this engine
+    uint64_t graph_captures = 0;  // chunk chains captured as CUDA graphs
+    // chunk chains run as captured CUDA graphs (QCG_GRAPH=0: direct launches)
+    static bool use_graphs() {
+        static const bool on = [] {
+            const char* e = std::getenv("QCG_GRAPH");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
     double host_wait_s = 0.0, host_prep_s = 0.0;  // lockstep loop: waiting vs preparing
     uint64_t host_steps = 0;
     double t_optimize_s = 0.0, t_final_s = 0.0, t_merge_s = 0.0, t_execute_s = 0.0;
