@@ -177,11 +177,13 @@ def test_identity_layers_in_multipass_chains(engine, oracle, q):
 
 @pytest.mark.parametrize("env", [{"QCG_PASS_B": "tma"},
                                  {"QCG_PASS_B": "tma", "QCG_B5_STORE": "stg"},
-                                 {"QCG_PASS_B": "v4"}],
-                         ids=["tma-tensor-store", "tma-register-store", "v4"])
+                                 {"QCG_PASS_B": "v4"},
+                                 {"QCG_GRAPH": "0", "QCG_PASS_A": "v4"}],
+                         ids=["tma-tensor-store", "tma-register-store", "v4", "direct-launch-v4-pass-a"])
 def test_pass_b_kernel_variants(env):
     """Every pass B kernel (qc_pass.cu: TMA boxes with tensor or register stores, v4
-    per-thread gathers) bit-exact at all geometry classes (tests/gpu_pass_variants.py)."""
+    per-thread gathers), and the chain without CUDA-graph capture and with the v4 pass A,
+    bit-exact at all geometry classes (tests/gpu_pass_variants.py)."""
     import os
     import subprocess
     import sys
