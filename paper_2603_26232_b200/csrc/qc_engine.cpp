@@ -371,7 +371,17 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             const uint64_t h0 = h2d, d0 = d2h;
             cudaGraph_t g = nullptr;
             QC_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-            ctx.glaunches = record(copy_bytes);
+            try {
+                ctx.glaunches = record(copy_bytes);
+            } catch (...) {  // never leave the stream in capture mode
+                cudaGraph_t bad = nullptr;
+                cudaStreamEndCapture(cs, &bad);
+                if (bad) cudaGraphDestroy(bad);
+                cudaGetLastError();
+                h2d = h0;
+                d2h = d0;
+                throw;
+            }
             QC_CUDA(cudaStreamEndCapture(cs, &g));
             QC_CUDA(cudaGraphInstantiate(&ctx.gexec, g, 0));
             QC_CUDA(cudaGraphDestroy(g));
