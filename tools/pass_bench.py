@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--p-edge", type=float, default=0.1)
+    ap.add_argument("--no-phase", action="store_true", help="gamma = 0: pass A without the phase")
     ap.add_argument("--per-launch", action="store_true",
                     help="also report pass_low us per rep (spread of a sporadic slow run)")
     a = ap.parse_args()
@@ -33,6 +34,8 @@ def main():
     rng = np.random.default_rng(0)
     idx = np.arange(a.slots, dtype=np.int32)
     prm = rng.uniform(0.1, 3.0, size=(a.slots, 2 * a.layers))
+    if a.no_phase:
+        prm[:, :a.layers] = 0.0
     ref = eng.eval_batch(graphs, a.layers, idx, prm)  # warm-up (+ first-touch)
     per = []
     if a.per_launch:
