@@ -244,3 +244,20 @@ def test_pipeline_c2_shape_matches_oracle(engine, oracle):
     assert got.cut == ref["cut"] and got.assignment == ref["assignment"]
     assert got.candidates_evaluated == ref["leaves"]
     assert np.array_equal(np.array([got.evals]), np.array([int(ref["sub_evals"].sum())]))
+
+
+def test_sweep_rows_match_oracle_pipeline(engine, oracle):
+    """paper_2603_26232_b200.sweep on the GPU: one CSV row per grid point, in the CLI's
+    axis order, with the cut the oracle's run_pipeline finds for the same instance."""
+    import io
+    from paper_2603_26232_b200.sweep import run_sweep
+    grid = {"qubits": 8, "layers": 1, "budget": 20, "n": [40], "p": [0.2, 0.4], "seed": [3],
+            "top_k": [2, 3]}
+    out = io.StringIO()
+    assert run_sweep(grid, out, engine=engine) == 4
+    rows = [r.split(",") for r in out.getvalue().splitlines()[1:]]
+    for row, (p, k) in zip(rows, [(0.2, 2), (0.2, 3), (0.4, 2), (0.4, 3)]):
+        e = oracle.generate_er(40, p, 3)
+        ref = oracle.run_pipeline(40, e, qubit_cap=8, top_k=k, layers=1, budget=20, seed=0)
+        assert row[0] == "40" and float(row[1]) == p and row[4] == str(k)
+        assert float(row[6]) == ref["cut"]
