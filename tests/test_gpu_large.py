@@ -57,3 +57,22 @@ def test_weighted_integral_c3_like(engine, oracle):
     ref = oracle.solve_subgraph(n, edges, top_k=3, layers=2, budget=40, seed=1, qubit_cap=24)
     got = engine.solve_subgraph(n, edges, top_k=3, layers=2, budget=40, seed=1, qubit_cap=24)
     assert np.array_equal(got.bits, ref.bits) and got.expectation == ref.expectation
+
+
+@pytest.mark.parametrize("q", [14, 20, 22])
+def test_large_lut_from_global_memory(engine, oracle26, q):
+    """Integer weights with a total above the pass kernels' shared-memory LUT cache (224
+    entries): the phase table is read from global memory (qc_pass.cu lut_sm == false).
+    Bit-exact amplitudes and expectation against the oracle, and eval_batch."""
+    rng = np.random.default_rng(q)
+    edges = [(u, v, float(rng.integers(20, 60))) for u in range(q) for v in range(u + 1, q)
+             if rng.random() < 0.25]
+    assert sum(w for _, _, w in edges) + 1 > 224
+    g = rng.uniform(0.05, 0.3, 2)
+    b = rng.uniform(0.1, 3.0, 2)
+    a0, x0 = oracle26.run_ansatz(q, edges, g, b, threads=THREADS)
+    a1, x1 = engine.run_ansatz(q, edges, g, b)
+    assert x1 == x0 and np.array_equal(a1, a0)
+    got = engine.eval_batch([(q, edges)], 2, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
+    assert got[0] == x0
+    del a0, a1
