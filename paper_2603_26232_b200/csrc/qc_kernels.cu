@@ -744,13 +744,21 @@ ChainPlan plan_chain(int q, bool sym) {
     for (int b = 12; b < Q; ++b) items.push_back(b);
     if (sym) items.push_back(-1);
     const uint32_t all = (Q == 32) ? ~0u : ((1u << Q) - 1u);
-    for (size_t i = 0; i < items.size(); i += kHighBits) {
+    // As few passes as the 9 gather bits allow, with the items spread evenly over them
+    // (e.g. 7 + 7 at 26 qubits rather than 9 + 5): a pass with <= 8 items needs 2
+    // register rounds instead of 3, and its free gather bits become pads that lengthen
+    // the contiguous runs each tile reads (measured: 9-target pass 4.4 TB/s vs a padded
+    // pass 5.6 TB/s at 24 qubits).
+    const size_t npass = (items.size() + kHighBits - 1) / kHighBits;
+    for (size_t i = 0, pi = 0; i < items.size(); ++pi) {
+        const size_t left = items.size() - i, passes_left = npass - pi;
+        const size_t take = (left + passes_left - 1) / passes_left;
         HighPass hp{};
         hp.mpos = -1;
         uint32_t single = 0x7u;  // column bits 0..2
         bool mirror = false;
         int k = 0;
-        for (; k < kHighBits && i + k < items.size(); ++k) {
+        for (; k < static_cast<int>(take); ++k) {
             const int it = items[i + k];
             if (it < 0) {
                 hp.mask[k] = all;
@@ -777,6 +785,7 @@ ChainPlan plan_chain(int q, bool sym) {
         }
         hp.freemask = freem;
         plan.high.push_back(hp);
+        i += take;
     }
     return plan;
 }

@@ -695,8 +695,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // of the launch's states: {16 doubles (column bits 0-2), targets, pads, low free run, high
 // free run x slots}; the mirror partners (x -> ~x) are a second 32 KB box at the
 // complemented free coordinates, whose elements sit in the box in reversed order. Box row
-// r = targets | pads << NT (128 bytes, 128-byte swizzle: unit u at u ^ (r & 7)). Under the
-// complement both the row and the column reverse, so the swizzled unit is unchanged:
+// r0 = pads | targets << NP (pads innermost: the copy walks the contiguous runs first;
+// 128 bytes per row, 128-byte swizzle: unit u at u ^ (r & 7)). Under the complement both
+// the row and the column reverse, so the swizzled unit is unchanged:
 //   byte(e) = m << 15 | (r0 ^ (m ? 255 : 0)) << 7 | ((w ^ r0) & 7) << 4.
 // Compute rounds are v4's; results go back to the same box positions and leave by tensor
 // stores of the same boxes (F_TSTORE), or straight from registers. Levels (f passes) still
@@ -710,13 +711,15 @@ struct B5Geo {
 
 template <int NT, int HM>
 __device__ __forceinline__ uint32_t pb5(uint32_t e) {
+    constexpr int NP = kHighBits - NT - HM;  // pads (the box's innermost row dimension)
     const uint32_t w = e & 7u, gb = e >> 3;
+    const uint32_t targets = gb & ((1u << NT) - 1u);
+    const uint32_t pads = gb >> (NT + HM);
+    const uint32_t r0 = pads | (targets << NP);
     if constexpr (HM == 0) {
-        return (gb << 7) | (((w ^ gb) & 7u) << 4);
+        return (r0 << 7) | (((w ^ r0) & 7u) << 4);
     } else {
-        constexpr uint32_t L = (1u << NT) - 1u;
         const uint32_t m = (gb >> NT) & 1u;
-        const uint32_t r0 = ((gb & L) | ((gb >> 1) & ~L)) & 255u;
         return (m << 15) | ((r0 ^ (0u - m)) & 255u) << 7 | (((w ^ r0) & 7u) << 4);
     }
 }
@@ -1149,17 +1152,20 @@ bool b5_plan(const HighPass& hp, int Q, B5Plan& P) {
     if (P.hm && hi_bits) return false;  // a mirror pass ends at the top stored bit
     P.geo = v4::B5Geo{static_cast<uint32_t>(lo), (1u << lo_bits) - 1u, static_cast<uint32_t>(hi),
                       (1u << hi_bits) - 1u, static_cast<uint32_t>(hi_bits), allq};
-    // dims: 0 columns, 1 targets (or their low 8), 2 pads (or the 9th target, or size 1),
-    // 3 low free run, 4 high free run x slots (size set per launch)
+    // dims: 0 columns, 1 pads (or the targets' low 8 when there are no pads), 2 targets
+    // (or the 9th target, or size 1), 3 low free run, 4 high free run x slots (size set
+    // per launch); row order = pb5's r0 = pads | targets << npad
     P.dims[0] = P.box[0] = 16;
-    P.dims[1] = P.box[1] = 1u << std::min(nt, 8);
-    P.strides[0] = nt ? (16ull << tstart) : 16ull;
-    if (nt == 9) {
-        P.dims[2] = P.box[2] = 2;
-        P.strides[1] = 16ull << (tstart + 8);
+    if (npad) {
+        P.dims[1] = P.box[1] = 1u << npad;
+        P.strides[0] = 128;
+        P.dims[2] = P.box[2] = 1u << nt;
+        P.strides[1] = nt ? (16ull << tstart) : 16ull;
     } else {
-        P.dims[2] = P.box[2] = 1u << npad;
-        P.strides[1] = 128;
+        P.dims[1] = P.box[1] = 1u << std::min(nt, 8);
+        P.strides[0] = 16ull << tstart;
+        P.dims[2] = P.box[2] = nt == 9 ? 2u : 1u;
+        P.strides[1] = nt == 9 ? (16ull << (tstart + 8)) : 16ull;
     }
     P.dims[3] = 1ull << lo_bits;
     P.box[3] = 1;
