@@ -689,7 +689,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// pass B, TMA variant (fp64, Q >= 21 by default; QCG_PASS_B=v4|tma forces a kernel).
+// pass B, TMA variant (fp64 at Q >= 21 and fp32 by default; QCG_PASS_B=v4|tma forces a
+// kernel). fp32 boxes have 64-byte rows (8 float2) under the 64-byte swizzle.
 // The 9 gather bits of a HighPass are [NT RX targets (one contiguous run of stored bits)]
 // [mirror, if HM] [pads: bits 3.. (contiguous)], so a tile is one box of a 5-D tensor view
 // of the launch's states: {16 doubles (column bits 0-2), targets, pads, low free run, high
@@ -709,31 +710,43 @@ struct B5Geo {
     uint32_t hi_bits, allq;       // allq: the Q stored-bit mask (mirror complement)
 };
 
-template <int NT, int HM>
+template <typename V, int NT, int HM>
 __device__ __forceinline__ uint32_t pb5(uint32_t e) {
     constexpr int NP = kHighBits - NT - HM;  // pads (the box's innermost row dimension)
     const uint32_t w = e & 7u, gb = e >> 3;
     const uint32_t targets = gb & ((1u << NT) - 1u);
     const uint32_t pads = gb >> (NT + HM);
     const uint32_t r0 = pads | (targets << NP);
-    if constexpr (HM == 0) {
-        return (r0 << 7) | (((w ^ r0) & 7u) << 4);
-    } else {
-        const uint32_t m = (gb >> NT) & 1u;
-        return (m << 15) | ((r0 ^ (0u - m)) & 255u) << 7 | (((w ^ r0) & 7u) << 4);
+    if constexpr (sizeof(V) == 16) {  // fp64: 128-byte rows, one amplitude per 16-byte unit
+        if constexpr (HM == 0) {
+            return (r0 << 7) | (((w ^ r0) & 7u) << 4);
+        } else {
+            const uint32_t m = (gb >> NT) & 1u;
+            return (m << 15) | ((r0 ^ (0u - m)) & 255u) << 7 | (((w ^ r0) & 7u) << 4);
+        }
+    } else {  // fp32: 64-byte rows, 64-byte swizzle (unit ^= row bits 1-2), two amps per unit
+        const uint32_t unit = ((w >> 1) ^ (r0 >> 1)) & 3u;
+        if constexpr (HM == 0) {
+            return (r0 << 6) | (unit << 4) | ((w & 1u) << 3);
+        } else {
+            // complement: row and column reverse; the swizzled unit is unchanged and only
+            // the amplitude inside the unit flips
+            const uint32_t m = (gb >> NT) & 1u;
+            return (m << 14) | ((r0 ^ (0u - m)) & 255u) << 6 | (unit << 4) | (((w & 1u) ^ m) << 3);
+        }
     }
 }
 
-template <int NT, int HM>
+template <typename V, int NT, int HM>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_b5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
               int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles,
               const __grid_constant__ B5Geo geo, const __grid_constant__ CUtensorMap tmap) {
-    using V = double2;
-    using A = Amp<double2>;
-    using S = double;
+    using A = Amp<V>;
+    using S = typename A::S;
+    constexpr uint32_t kHalf = sizeof(V) == 16 ? 32768u : 16384u;  // bytes of a mirror box
     extern __shared__ __align__(1024) unsigned char sm_raw[];
-    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // 128B swizzle
+    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // swizzle atoms
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
@@ -796,11 +809,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             sxb[s] = xb;
             tag[s] = k;
             if (act) {
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(65536u)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(2u * kHalf)
                              : "memory");
                 const uint32_t sdst = su32(sm + s * kStageAmpBytes);
                 tma(false, sdst, xb, t >> tshift, bar);
-                if (HM) tma(false, sdst + 32768u, xb ^ geo.allq, t >> tshift, bar);
+                if (HM) tma(false, sdst + kHalf, xb ^ geo.allq, t >> tshift, bar);
             } else {
                 bar_arrive(bar);
             }
@@ -848,14 +861,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nrr = mix ? nr : 1;
         const uint32_t xs = sxb[s];
         const uint32_t xb = xs | w;
-        const S c = d.c, sn = d.s;
+        const S c = static_cast<S>(d.c), sn = static_cast<S>(d.s);
         unsigned char* stb = sm + s * kStageAmpBytes;
         const uint16_t* slev = reinterpret_cast<const uint16_t*>(sm + kOffLev + s * 8192u);
-        S* const gf = d.fbuf;
+        S* const gf = reinterpret_cast<S*>(d.fbuf);  // f(z) in the amplitude precision
         const uint16_t* const glev = d.lev;
         const double* const gval = d.val;
         V a[16];
-        auto at = [&](uint32_t e) -> V& { return *reinterpret_cast<V*>(stb + pb5<NT, HM>(e)); };
+        auto at = [&](uint32_t e) -> V& { return *reinterpret_cast<V*>(stb + pb5<V, NT, HM>(e)); };
         auto e_of = [&](auto R, int j) -> uint32_t {
             if constexpr (decltype(R)::value == 0)
                 return w | (static_cast<uint32_t>(j) << 3) | ((gt >> 3) << 7);
@@ -886,7 +899,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (glev)
                             cst = static_cast<S>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
                         else
-                            cst = gval ? gval[gidx] : 1.0;
+                            cst = static_cast<S>(gval ? gval[gidx] : 1.0);
                         gf[gidx] = A::mul(A::nrm(a[j]), cst);
                     }
                 }
@@ -904,7 +917,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (glev)
                         cst = static_cast<S>(slev[(e_of(R, j) >> 3) * 8u + (gidx & 7u)]);
                     else
-                        cst = gval ? gval[gidx] : 1.0;
+                        cst = static_cast<S>(gval ? gval[gidx] : 1.0);
                     gf[gidx] = A::mul(A::nrm(a[j]), cst);  // stays in L2 for k_blocksum
                 }
             }
@@ -916,7 +929,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (gt == 0) {
                     const uint32_t sb = su32(stb);
                     tma(true, sb, xs, t >> tshift, 0);
-                    if (HM) tma(true, sb + 32768u, xs ^ geo.allq, t >> tshift, 0);
+                    if (HM) tma(true, sb + kHalf, xs ^ geo.allq, t >> tshift, 0);
                     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                 }
                 pending = k + kStages;
@@ -1072,38 +1085,42 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
 namespace {
 using B5Kernel = void (*)(const SlotDesc*, const LayerParam*, int, int, HighPass, uint32_t, uint32_t,
                           v4::B5Geo, CUtensorMap);
-template <int NT, int HM>
+template <typename V, int NT, int HM>
 B5Kernel b5_kernel() {
     static bool attr = false;
     if (!attr) {
-        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b5<NT, HM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b5<V, NT, HM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(v4::kSmem + 1024)));
         attr = true;
     }
-    return v4::k_pass_b5<NT, HM>;
+    return v4::k_pass_b5<V, NT, HM>;
 }
-B5Kernel b5_lookup(int nt, int hm) {
+template <typename V>
+B5Kernel b5_lookup_t(int nt, int hm) {
     switch (nt * 2 + hm) {
-        case 1: return b5_kernel<0, 1>();
-        case 2: return b5_kernel<1, 0>();
-        case 3: return b5_kernel<1, 1>();
-        case 4: return b5_kernel<2, 0>();
-        case 5: return b5_kernel<2, 1>();
-        case 6: return b5_kernel<3, 0>();
-        case 7: return b5_kernel<3, 1>();
-        case 8: return b5_kernel<4, 0>();
-        case 9: return b5_kernel<4, 1>();
-        case 10: return b5_kernel<5, 0>();
-        case 11: return b5_kernel<5, 1>();
-        case 12: return b5_kernel<6, 0>();
-        case 13: return b5_kernel<6, 1>();
-        case 14: return b5_kernel<7, 0>();
-        case 15: return b5_kernel<7, 1>();
-        case 16: return b5_kernel<8, 0>();
-        case 17: return b5_kernel<8, 1>();
-        case 18: return b5_kernel<9, 0>();
+        case 1: return b5_kernel<V, 0, 1>();
+        case 2: return b5_kernel<V, 1, 0>();
+        case 3: return b5_kernel<V, 1, 1>();
+        case 4: return b5_kernel<V, 2, 0>();
+        case 5: return b5_kernel<V, 2, 1>();
+        case 6: return b5_kernel<V, 3, 0>();
+        case 7: return b5_kernel<V, 3, 1>();
+        case 8: return b5_kernel<V, 4, 0>();
+        case 9: return b5_kernel<V, 4, 1>();
+        case 10: return b5_kernel<V, 5, 0>();
+        case 11: return b5_kernel<V, 5, 1>();
+        case 12: return b5_kernel<V, 6, 0>();
+        case 13: return b5_kernel<V, 6, 1>();
+        case 14: return b5_kernel<V, 7, 0>();
+        case 15: return b5_kernel<V, 7, 1>();
+        case 16: return b5_kernel<V, 8, 0>();
+        case 17: return b5_kernel<V, 8, 1>();
+        case 18: return b5_kernel<V, 9, 0>();
         default: return nullptr;
     }
+}
+B5Kernel b5_lookup(int nt, int hm, bool fp32) {
+    return fp32 ? b5_lookup_t<float2>(nt, hm) : b5_lookup_t<double2>(nt, hm);
 }
 
 // HighPass -> 5-D box geometry of k_pass_b5 over a launch's contiguous states. False if
@@ -1115,7 +1132,8 @@ struct B5Plan {
     cuuint64_t strides[4];
     cuuint32_t box[5];
 };
-bool b5_plan(const HighPass& hp, int Q, B5Plan& P) {
+bool b5_plan(const HighPass& hp, int Q, bool fp32, B5Plan& P) {
+    const cuuint64_t ab = fp32 ? 8 : 16;  // bytes per amplitude
     int nt = 0, npad = 0, tstart = -1;
     uint32_t tmask = 0, pmask = 0;
     for (int b = 0; b < kHighBits; ++b) {
@@ -1158,33 +1176,34 @@ bool b5_plan(const HighPass& hp, int Q, B5Plan& P) {
     P.dims[0] = P.box[0] = 16;
     if (npad) {
         P.dims[1] = P.box[1] = 1u << npad;
-        P.strides[0] = 128;
+        P.strides[0] = 8 * ab;
         P.dims[2] = P.box[2] = 1u << nt;
-        P.strides[1] = nt ? (16ull << tstart) : 16ull;
+        P.strides[1] = nt ? (ab << tstart) : 16ull;
     } else {
         P.dims[1] = P.box[1] = 1u << std::min(nt, 8);
-        P.strides[0] = 16ull << tstart;
+        P.strides[0] = ab << tstart;
         P.dims[2] = P.box[2] = nt == 9 ? 2u : 1u;
-        P.strides[1] = nt == 9 ? (16ull << (tstart + 8)) : 16ull;
+        P.strides[1] = nt == 9 ? (ab << (tstart + 8)) : 16ull;
     }
     P.dims[3] = 1ull << lo_bits;
     P.box[3] = 1;
-    P.strides[2] = 16ull << lo;
+    P.strides[2] = ab << lo;
     P.box[4] = 1;
-    P.strides[3] = 16ull << hi;
-    return (nt + P.hm + npad) == kHighBits && b5_lookup(nt, P.hm) != nullptr;
+    P.strides[3] = ab << hi;
+    return (nt + P.hm + npad) == kHighBits && b5_lookup(nt, P.hm, fp32) != nullptr;
 }
-// fp64 pass B kernel: the TMA kernel (tensor stores) where it measured faster, Q >= 21
-// (q=24: -3.5%, q=26: -4.1% per launch); at Q <= 19 v4's per-thread gathers are as fast
-// or faster (profiles/r1_pass_b_tma.txt). QCG_PASS_B=v4|tma forces one.
-bool tma_pass_b(int Q) {
+// Pass B kernel: the TMA kernel (tensor stores) where it measured faster: fp64 at Q >= 21
+// (at Q <= 19 v4's per-thread gathers are as fast or faster), fp32 at every size (v4 moves
+// fp32 in 8-byte cp.async / STG per amplitude: q=20 65 -> 54 us, q=26 372 -> 255 us)
+// (profiles/r1_pass_b_tma.txt). QCG_PASS_B=v4|tma forces one.
+bool tma_pass_b(int Q, bool fp32) {
     static const int mode = [] {
         const char* e = std::getenv("QCG_PASS_B");
         if (e && std::string(e) == "v4") return 0;
         if (e && std::string(e) == "tma") return 1;
         return 2;
     }();
-    return mode == 1 || (mode == 2 && Q >= 21);
+    return mode == 1 || (mode == 2 && (fp32 || Q >= 21));
 }
 }  // namespace
 
@@ -1195,12 +1214,12 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     const bool fp32 = flags & F_FP32;
     int launches = 0;
     B5Plan P;
-    if (tma_pass_b(Q) && !fp32 && state_base && b5_plan(hp, Q, P)) {
+    if (tma_pass_b(Q, fp32) && state_base && b5_plan(hp, Q, fp32, P)) {
         static const bool tstore = [] {  // QCG_B5_STORE=stg: results leave from registers
             const char* e = std::getenv("QCG_B5_STORE");
             return !(e && std::string(e) == "stg");
         }();
-        const B5Kernel kern = b5_lookup(P.nt, P.hm);
+        const B5Kernel kern = b5_lookup(P.nt, P.hm, fp32);
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
@@ -1209,9 +1228,10 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
             CUtensorMap tm;
             const cuuint32_t es[5] = {1, 1, 1, 1, 1};
             const CUresult r = tensor_encoder()(
-                &tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
-                const_cast<char*>(static_cast<const char*>(state_base)) + (static_cast<size_t>(s0) << Q) * 16,
-                P.dims, P.strides, P.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                &tm, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5,
+                const_cast<char*>(static_cast<const char*>(state_base)) + (static_cast<size_t>(s0) << Q) * (fp32 ? 8 : 16),
+                P.dims, P.strides, P.box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                fp32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) internal_error("pass B tensor map: " + std::to_string(static_cast<int>(r)));
             launch_ex(kern, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream, pdl || s0 > 0,
