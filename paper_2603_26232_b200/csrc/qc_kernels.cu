@@ -316,19 +316,31 @@ __global__ void __launch_bounds__(kFsumThreads) k_fsum_f32(const float* __restri
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
+    __shared__ unsigned last;
+    double* pp = partials + static_cast<size_t>(slot) * nbl;
     if (threadIdx.x == 0) {
         double t = 0.0;
         for (int w = 0; w < kFsumThreads / 32; ++w) t += red[w];
-        double* pp = partials + static_cast<size_t>(slot) * nbl;
         pp[b] = t;
         __threadfence();
-        if (atomicAdd(&tickets[slot], 1u) == static_cast<unsigned>(nbl - 1)) {
-            __threadfence();
-            double total = 0.0;
-            for (int k = 0; k < nbl; ++k) total += __ldcg(pp + k);
-            out[slot] = sym ? 2.0 * total : total;
-            tickets[slot] = 0u;
-        }
+        last = atomicAdd(&tickets[slot], 1u) == static_cast<unsigned>(nbl - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    // the slot's last CTA: every thread adds a strided share of the partials (fp32 mode
+    // has no summation-order contract; up to 2^14 partials at 26 qubits)
+    __threadfence();
+    double t = 0.0;
+    for (int k = threadIdx.x; k < nbl; k += kFsumThreads) t += __ldcg(pp + k);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    __syncthreads();  // red[] reuse
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double total = 0.0;
+        for (int w = 0; w < kFsumThreads / 32; ++w) total += red[w];
+        out[slot] = sym ? 2.0 * total : total;
+        tickets[slot] = 0u;
     }
 }
 
