@@ -304,16 +304,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // a 1-D bulk copy the levels; results are staged linearly in the same stage and leave by
 // one 64 KB bulk store, after which the lane refills the stage.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t ph5(uint32_t e) {  // tile index -> 16-byte unit
+// tile index -> amplitude slot in the stage. fp64: 128-byte rows r = m + 256*half, 128-byte
+// swizzle (16-byte unit u at u ^ (r & 7)); fp32: 64-byte rows, 64-byte swizzle (16-byte
+// unit = two amplitudes, at unit ^ ((r >> 1) & 3)).
+template <typename V>
+__device__ __forceinline__ uint32_t ph5(uint32_t e) {
     const uint32_t m = e >> 4, half = (e >> 3) & 1u, u = e & 7u;
-    return ((m + (half << 8)) << 3) | (u ^ (m & 7u));
+    const uint32_t r = m + (half << 8);
+    if constexpr (sizeof(V) == 16)
+        return (r << 3) | (u ^ (m & 7u));
+    else
+        return (r << 3) | ((((u >> 1) ^ (r >> 1)) & 3u) << 1) | (u & 1u);
 }
 
+template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_a5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
               int Q, uint32_t flags, uint32_t total_tiles, const __grid_constant__ CUtensorMap tmap) {
-    using V = double2;
-    using A = Amp<double2>;
+    using A = Amp<V>;
+    using S = typename A::S;
+    constexpr uint32_t kTileBytes = 4096u * sizeof(V);
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // TMA 128B swizzle
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
@@ -349,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tag[s] = k;
         const bool lv = d.phase && d.lev;
         if (init || d.phase || d.mix) {
-            const uint32_t bytes = (init ? 0u : 65536u) + (lv ? 8192u : 0u);
+            const uint32_t bytes = (init ? 0u : kTileBytes) + (lv ? 8192u : 0u);
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
                          : "memory");
             if (!init)
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int jj = 0; jj < 8; ++jj) {
                     const int j = h * 8 + jj;
                     const uint32_t e = gt * 16u + j;
-                    V v = init ? A::mk(amp0, 0.0) : st[ph5(e)];
+                    V v = init ? A::mk(static_cast<S>(amp0), S(0)) : st[ph5<V>(e)];
                     if (phase) {
                         if (use_lev) {
                             const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
@@ -436,20 +446,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (mix) rx_local<V, 0, 4>(a, c, sn);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st[ph5(gt * 16u + j)] = a[j];
+            for (int j = 0; j < 16; ++j) st[ph5<V>(gt * 16u + j)] = a[j];
         }
         __syncwarp();  // round 1 reads only what its own half-warp wrote (e>>8 = gt>>4)
         {
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) a[j] = st[ph5(r | (j << 4))];
+            for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>(r | (j << 4))];
             if (mix) rx_local<V, 0, 4>(a, c, sn);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) st[ph5(r | (j << 4))] = a[j];
+            for (int j = 0; j < 16; ++j) st[ph5<V>(r | (j << 4))] = a[j];
         }
         grp_sync(g);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a[j] = st[ph5((j << 8) | gt)];
+        for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>((j << 8) | gt)];
         grp_sync(g);  // the stage's tile is in registers: it becomes the output staging
         if (mix) rx_local<V, 0, 4>(a, c, sn);
 #pragma unroll
@@ -457,9 +467,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         grp_sync(g);
         if (gt == 0) {
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 65536;\n" ::"l"(
-                             d.state + base),
-                         "r"(su32(st))
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                             reinterpret_cast<V*>(d.state) + base),
+                         "r"(su32(st)), "r"(kTileBytes)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
         }
@@ -1019,25 +1029,42 @@ EncodeTiledFn5 tensor_encoder() {
     }
     return encode;
 }
-CUtensorMap state_tensor_map(const void* base, uint64_t amps) {
+// {16 scalars (8 amplitudes), 16-amplitude groups, 2 halves}; fp32 rows are 64 bytes
+CUtensorMap state_tensor_map(const void* base, uint64_t amps, bool fp32 = false) {
     const EncodeTiledFn5 encode = tensor_encoder();
     CUtensorMap m;
+    const cuuint64_t ab = fp32 ? 8 : 16;
     const cuuint64_t dims[3] = {16, amps / 16, 2};
-    const cuuint64_t strides[2] = {256, 128};
+    const cuuint64_t strides[2] = {16 * ab, 8 * ab};
     const cuuint32_t box[3] = {16, 256, 2};
     const cuuint32_t es[3] = {1, 1, 1};
-    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims,
-                              strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    const CUresult r = encode(&m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                              const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              fp32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) internal_error("state tensor map: " + std::to_string(static_cast<int>(r)));
     return m;
 }
-bool tma_pass_a() {  // default for fp64; QCG_PASS_A=v4 selects the cp.async/STG version
-    static const bool on = [] {
+// TMA pass A: default for fp64, and for fp32 at Q >= 21 (fp32 per launch with 2-4 slots:
+// q=24 161.9 -> 146.1 us, q=26 313 -> 276; q=20 60.6 -> 58.8 but the C2 bench is 1% slower;
+// the C3/C5 fp32 solves are unchanged); QCG_PASS_A=v4|tma forces one kernel
+bool tma_pass_a(bool fp32, int Q) {
+    static const int mode = [] {
         const char* e = std::getenv("QCG_PASS_A");
-        return !(e && std::string(e) == "v4");
+        if (e && std::string(e) == "v4") return 0;
+        if (e && std::string(e) == "tma") return 1;
+        return 2;
     }();
-    return on;
+    return mode == 1 || (mode == 2 && (!fp32 || Q >= 21));
+}
+template <typename V>
+void a5_attr() {
+    static bool attr = false;
+    if (!attr) {
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kSmem + 1024)));
+        attr = true;
+    }
 }
 }  // namespace
 
@@ -1045,23 +1072,25 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
                    int n_slots, cudaStream_t stream, bool pdl, const void* state_base) {
     const int sms = sm_count();
     const bool fp32 = flags & F_FP32;
-    if (tma_pass_a() && !fp32 && state_base) {
-        static bool attr = false;
-        if (!attr) {
-            QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(v4::kSmem + 1024)));
-            attr = true;
-        }
+    if (tma_pass_a(fp32, Q) && state_base) {
+        if (fp32)
+            a5_attr<float2>();
+        else
+            a5_attr<double2>();
         int launches = 0;
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
             const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
             const CUtensorMap tm = state_tensor_map(
-                static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * 16,
-                static_cast<uint64_t>(n) << Q);
-            launch_ex(v4::k_pass_a5, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
-                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
+                static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * (fp32 ? 8 : 16),
+                static_cast<uint64_t>(n) << Q, fp32);
+            if (fp32)
+                launch_ex(v4::k_pass_a5<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
+                          pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
+            else
+                launch_ex(v4::k_pass_a5<double2>, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
+                          pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
             ++launches;
         }
         return launches;
