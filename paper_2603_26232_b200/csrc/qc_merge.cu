@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(SearchArgs A, uint64_
 
     if (idx0 < T) {
         int r[kMaxL], c[kMaxL], sel[kMaxL];
-        int64_t ips[kMaxL];
-        double dps[kMaxL];
+        int64_t ips[kMaxL] = {};  // score_level fills them in level order
+        double dps[kMaxL] = {};
         // decode idx0
         uint64_t rem = idx0;
         int need = need0;
