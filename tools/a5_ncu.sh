@@ -1,3 +1,4 @@
+# ncu --set full capture of the TMA pass A at the C2 shape (gpurun_out/a5_q20.ncu-rep)
 set -u
 O=gpurun_out; mkdir -p $O
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:'k_pass_a5' -c 3 \

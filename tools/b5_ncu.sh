@@ -1,3 +1,4 @@
+# ncu --set full captures of pass B (TMA and v4) at the C2 shape
 set -u
 O=gpurun_out; mkdir -p $O
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:'k_pass_b' -c 4 \
