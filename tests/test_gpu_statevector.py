@@ -191,3 +191,16 @@ def test_pass_b_kernel_variants(env):
     r = subprocess.run([sys.executable, os.path.join(here, "gpu_pass_variants.py")],
                        env={**os.environ, **env}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_split_launches():
+    """Passes split into several persistent launches (slot offsets in the tensor maps):
+    tests/gpu_many_slots.py with one chunk and the TMA pass B forced."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = {**os.environ, "QCG_CHUNKS": "1", "QCG_PASS_B": "tma"}
+    r = subprocess.run([sys.executable, os.path.join(here, "gpu_many_slots.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-2000:]
