@@ -147,7 +147,7 @@ def test_duplicate_edges_rejected_like_add_edge(engine, n):
         assert integral and mx == 2.0
 
 
-@pytest.mark.parametrize("q,layers", [(10, 1), (14, 2), (20, 2)])
+@pytest.mark.parametrize("q,layers", [(10, 1), (14, 2), (20, 2), (22, 1), (24, 1)])
 def test_fractional_weights_within_tolerance(engine, oracle, q, layers):
     """Non-integral weights take statevector.hpp:162-164 (per-amplitude std::polar). The
     device evaluates sin/cos itself; glibc's sin/cos are not correctly rounded (~0.13% of
@@ -158,10 +158,13 @@ def test_fractional_weights_within_tolerance(engine, oracle, q, layers):
     e["w"] = rng.uniform(0.1, 1.1, len(e))
     g = rng.uniform(0.2, np.pi, layers)
     b = rng.uniform(0.2, np.pi, layers)
-    a0, x0 = oracle.run_ansatz(q, e, g, b)
+    a0, x0 = oracle.run_ansatz(q, e, g, b, threads=max(1, min(32, __import__("os").cpu_count() or 1)))
     a1, x1 = engine.run_ansatz(q, e, g, b)
     assert abs(x1 - x0) <= 1e-10 * abs(x0)
     assert np.max(np.abs(a1 - a0)) <= 1e-10 * np.max(np.abs(a0))
+    # the half-state eval path (value-table f in the last pass, TMA kernels at q >= 22)
+    got = engine.eval_batch([(q, e)], layers, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
+    assert abs(got[0] - x0) <= 1e-10 * abs(x0)
 
 
 @pytest.mark.parametrize("q", [14, 20])
