@@ -207,3 +207,19 @@ def test_split_launches():
     r = subprocess.run([sys.executable, os.path.join(here, "gpu_many_slots.py")], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_graph_replay_across_graphs_and_shapes(engine, oracle):
+    """Chunk steps replay captured CUDA graphs keyed by shape and buffers; the graphs
+    evaluated travel in the staging copy. Alternate different graphs of the same shape
+    and a different shape on one engine: every result must match the oracle bit for bit."""
+    rng = np.random.default_rng(7)
+    ga = oracle.generate_er(16, 0.3, 1)
+    gb = oracle.generate_er(16, 0.5, 2)
+    gc = oracle.generate_er(18, 0.3, 3)
+    for q, e in [(16, ga), (16, gb), (18, gc), (16, ga), (16, gb), (18, gc)]:
+        prm = rng.uniform(0.1, 3.0, size=(3, 4))
+        got = engine.eval_batch([(q, e)], 2, np.zeros(3, np.int32), prm)
+        for k in range(3):
+            x0 = oracle.run_ansatz(q, e, prm[k, :2], prm[k, 2:], want_amps=False)[1]
+            assert got[k] == x0, (q, k, got[k], x0)
