@@ -217,6 +217,45 @@ def run_reference_arm(args, w):
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
+def steady_state(eng, w, kernel, slots=(10, 40), reps=3):
+    """The dominant pass kernel at two batch sizes of the workload's subgraph shape (one
+    chunk, one stream, every launch timed by CUDA events): time per launch = fixed +
+    slots x slope, so the steady-state bandwidth is bytes-per-slot / slope. Separates the
+    per-launch fixed cost (launch, ring fill, drain) from the streaming efficiency."""
+    from paper_2603_26232_b200 import generate_er
+    q, p = w["qubit_cap"], w["layers"]
+    e = generate_er(q, 0.2, 1)
+    rng = np.random.default_rng(0)
+    prev = os.environ.get("QCG_CHUNKS")
+    os.environ["QCG_CHUNKS"] = "1"
+    pts = []
+    try:
+        for n in slots:
+            prm = rng.uniform(0.1, 3.0, size=(n, 2 * p))
+            idx = np.zeros(n, np.int32)
+            eng.eval_batch([(q, e)], p, idx, prm)  # warm (buffers, graph capture)
+            eng.profile(1)
+            for _ in range(reps):
+                eng.eval_batch([(q, e)], p, idx, prm)
+            v = eng.profile_read()[kernel]
+            eng.profile(False)
+            if not v["launches"]:
+                return None
+            pts.append((n, v["ms"] * 1e3 / v["launches"], v["bytes"] / v["launches"]))
+    finally:
+        if prev is None:
+            os.environ.pop("QCG_CHUNKS", None)
+        else:
+            os.environ["QCG_CHUNKS"] = prev
+    (n1, t1, b1), (n2, t2, b2) = pts
+    slope = (t2 - t1) / (n2 - n1)                  # us per slot
+    per_slot = b2 / n2                             # algorithmic bytes per slot and launch
+    return {"kernel": kernel, "subgraph_qubits": q, "slots": [n1, n2],
+            "us_per_launch": [round(t1, 2), round(t2, 2)], "us_per_slot": round(slope, 3),
+            "fixed_us_per_launch": round(t1 - n1 * slope, 2),
+            "achieved": per_slot / (slope * 1e-6) / 1e9 if slope > 0 else None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -393,6 +432,14 @@ def main():
         pass
     fp64_peak = FP64_PEAK_TOPS
     fp64_ach = d.get("fp64_ops", 0.0) / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
+    ss = None
+    if world == 1 and dom in ("pass_low", "pass_high"):
+        try:
+            ss = steady_state(eng, w, dom)
+            if ss and ss.get("achieved"):
+                ss["frac"] = ss["achieved"] / peak
+        except Exception as ex:  # diagnostic only: never fail the bench on it
+            ss = {"error": str(ex)[:200]}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind ==
@@ -402,6 +449,8 @@ def main():
                 "measured": "every launch of one single-stream step, CUDA events on its stream",
                 "launches": d["launches"],
                 "share_of_step": d["ms"] / iso_ms if iso_ms else None,
+                # streaming efficiency without the per-launch fixed cost (see steady_state)
+                "steady_state": ss,
                 # the fp64 parity path forbids FMA: every butterfly is 8 DMUL + 4 DADD, so
                 # the FP64 pipe is the second ceiling (co-bound for the 12-target pass A)
                 "fp64": {"achieved_tops": fp64_ach, "peak_tops": fp64_peak,
