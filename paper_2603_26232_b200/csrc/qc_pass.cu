@@ -657,6 +657,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         };
         auto finish = [&](auto R) {
+            if (fout && glev && !(flags & F_NOLEVREG)) {
+                // f pass: take this thread's 16 cut levels into registers (two per word)
+                // so the stage can be refilled before the f(z) stores, like the other passes
+                constexpr int r = decltype(R)::value;
+                const uint32_t txt = r == 0 ? hx(hp, (gt >> 3) << 4)
+                                   : r == 1 ? hx(hp, ((gt >> 3) & 15u) | ((gt >> 7) << 8))
+                                            : hx(hp, (gt >> 3) << 3);
+                const uint32_t xt = xb ^ txt;
+                uint32_t lvp[8];
+#pragma unroll
+                for (int j = 0; j < 16; j += 2) {
+                    const uint32_t g0 = xt ^ hx(hp, gb_local<r>(j));
+                    const uint32_t g1 = xt ^ hx(hp, gb_local<r>(j + 1));
+                    lvp[j >> 1] = static_cast<uint32_t>(slev[(e_of(R, j) >> 3) * 8u + (g0 & 7u)]) |
+                                  (static_cast<uint32_t>(slev[(e_of(R, j + 1) >> 3) * 8u + (g1 & 7u)]) << 16);
+                }
+                grp_sync(g);
+                issue(k + kStages);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t gidx = xt ^ hx(hp, gb_local<r>(j));
+                    if (sout) __stcs(gstate + gidx, a[j]);
+                    const S cst = static_cast<S>((lvp[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+                    gf[gidx] = Amp<V>::mul(Amp<V>::nrm(a[j]), cst);
+                }
+                return;
+            }
             grp_sync(g);
             if (!fout) issue(k + kStages);  // f reads the stage's levels: refill after
             emit(R);
@@ -1273,12 +1300,16 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
         const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+        static const uint32_t nolev = [] {
+            const char* e = std::getenv("QCG_LEVREG");
+            return (e && e[0] == '0') ? static_cast<uint32_t>(F_NOLEVREG) : 0u;
+        }();
         if (fp32)
             launch_ex(v4::k_pass_b<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
-                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags, tiles);
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags | nolev, tiles);
         else
             launch_ex(v4::k_pass_b<double2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
-                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags, tiles);
+                      pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, hp, flags | nolev, tiles);
         ++launches;
     }
     return launches;
