@@ -389,6 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lut_owner = -1;
     int pending = -1;  // local tile whose refill waits on this group's last bulk store
     for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        // refill the stage of this group's previous tile as soon as its bulk store has read
+        // it, before waiting for this tile's data
+        if (pending >= 0) {
+            if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            issue(pending);
+            pending = -1;
+        }
         const int s = k % kStages;
         const uint32_t t = t0 + static_cast<uint32_t>(k);
         const PD& d = pd[(t >> tshift) - sa];
@@ -404,11 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (tag[s] != k) {
         }
         bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
-        if (pending >= 0) {
-            if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-            issue(pending);
-            pending = -1;
-        }
         if (!act) {
             grp_sync(g);
             issue(k + kStages);
