@@ -63,6 +63,7 @@ enum : uint32_t {
     F_SYM = 8u,         // half-state storage (complement symmetry), else full state
     F_FP32 = 64u,       // optional fp32 mode: float2 amplitudes, float f(z), fp32 LUTs (1e-4)
     F_TSTORE = 128u,    // pass B (TMA): results leave by tensor stores (default)
+    F_B5EARLY = 512u,   // pass B (TMA): refill a stored stage before the next tile's wait
     F_NOLEVREG = 256u,  // pass B (v4) f pass: levels read after the refill (experiment)
 };
 

@@ -792,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
     const bool tstore = flags & F_TSTORE;  // results leave by tensor stores of the boxes
+    const bool early = flags & F_B5EARLY;  // experiment: refill before the next tile's wait
     uint32_t t0;
     int cnt;
     tile_range(total_tiles, t0, cnt);
@@ -884,6 +885,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t t = t0 + static_cast<uint32_t>(k);
         const PD& d = pd[(t >> tshift) - sa];
         const bool mix = d.mix;
+        if (pending >= 0 && early) {  // refill the previous tile's stage once its store has read it
+            if (gt == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+            issue(pending);
+            pending = -1;
+        }
         while (tag[s] != k) {
         }
         bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
@@ -1292,8 +1298,16 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
                 fp32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) internal_error("pass B tensor map: " + std::to_string(static_cast<int>(r)));
+            // refill a stored stage before waiting for the next tile: measured faster at 26
+            // qubits (8 slots 1541 -> 1502 us), slower at 24 (22 slots 975 -> 988 us);
+            // QCG_B5_EARLY=0|1 forces it
+            static const int early_env = [] {
+                const char* e = std::getenv("QCG_B5_EARLY");
+                return e ? (e[0] == '1' ? 1 : 0) : -1;
+            }();
+            const uint32_t early = (early_env == 1 || (early_env < 0 && Q >= 25)) ? static_cast<uint32_t>(F_B5EARLY) : 0u;
             launch_ex(kern, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream, pdl || s0 > 0,
-                      d_slots + s0, d_lp, layer, Q, hp, flags | (tstore ? F_TSTORE : 0u), tiles, P.geo, tm);
+                      d_slots + s0, d_lp, layer, Q, hp, flags | (tstore ? F_TSTORE : 0u) | early, tiles, P.geo, tm);
             ++launches;
         }
         return launches;
