@@ -217,7 +217,7 @@ def run_reference_arm(args, w):
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
-def steady_state(eng, w, kernel, slots=(10, 40), reps=3):
+def steady_state(eng, w, kernel, slots=(10, 40), reps=8):
     """The dominant pass kernel at two batch sizes of the workload's subgraph shape (one
     chunk, one stream, every launch timed by CUDA events): time per launch = fixed +
     slots x slope, so the steady-state bandwidth is bytes-per-slot / slope. Separates the
