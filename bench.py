@@ -154,64 +154,245 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------
 # CPU baseline / reference arm
 # --------------------------------------------------------------------------------------
-def reference_sample(w, edges, budgets=(4, 12)):
-    """Time the reference pipeline (partition -> QAOA stage -> merge, all host threads) at
-    two small NM budgets and extrapolate the QAOA stage linearly to the full budget
-    (fixed per-subgraph costs — cost table, final circuit, top-K — are the intercept).
-    Returns (evals/s, description, kind, cores, seconds spent)."""
+def host_info():
+    """CPU model, logical cores and memory of this host (the reference arm's hardware)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    mem = None
+    try:
+        with open("/proc/meminfo") as f:
+            mem = round(int(f.readline().split()[1]) / 2**20, 1)
+    except (OSError, ValueError, IndexError):
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_gib": mem}
+
+
+def subgraph_count(w):
+    """partition.hpp:163-167 derive_subgraph_count (the chain split both arms use)."""
+    n, cap = w["n"], w["qubit_cap"]
+    return 1 if n <= cap else (n - 1 + cap - 2) // (cap - 1)
+
+
+def config_dict(w, world):
+    """The workload description; identical in both arms (same keys, same values)."""
+    return {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
+            "graph": "weighted random 3-regular" if "regular" in w else "Erdos-Renyi",
+            "qubit_cap": w["qubit_cap"], "subgraphs": subgraph_count(w), "layers": w["layers"],
+            "top_k": w["top_k"], "budget": w["budget"], "seed": w["seed"],
+            "parallelism": f"shard{world}"}
+
+
+# Workloads whose full reference solve fits a bench run (C1 ~0.2 s, C2 ~27 s on 16 host
+# threads). The others take minutes to hours on the CPU (C3 ~8 min, C4 ~2 h, C5 ~days),
+# so their reference numbers come from a bounded sample of the same QAOA stage.
+FULL_REFERENCE = ("c1", "c2")
+# sampled reference: NM budget per sampled solve (the ramp eval + the first simplex points)
+SAMPLE_BUDGET = {"c3": 4, "c4": 40, "c5": 2}
+
+
+def ref_lib(w):
     from oracle.refpy import OracleLib, RefLib, ref_available
-    kind = "reference" if ref_available() else "port"
-    lib = RefLib() if kind == "reference" else OracleLib()
-    cores = os.cpu_count() or 1
-    t0 = time.time()
-    runs = []
-    for b in budgets:
-        r = lib.run_pipeline(w["n"], edges, qubit_cap=w["qubit_cap"], top_k=w["top_k"],
-                             layers=w["layers"], budget=b, seed=0, workers=cores)
-        runs.append(r)
-    (b1, r1), (b2, r2) = zip(budgets, runs)
-    slope = max((r2["qaoa_s"] - r1["qaoa_s"]) / (b2 - b1), 0.0)
-    fixed = max(r1["qaoa_s"] - slope * b1, 0.0)
-    qaoa_full = fixed + slope * w["budget"]
-    merge_s = min(r1["merge_s"], r2["merge_s"])
-    total = r1["partition_s"] + qaoa_full + merge_s
-    M = r1["subgraphs"]
-    value = M * w["budget"] / total
-    desc = (f"{'oracle/_ref (unmodified qcut headers)' if kind == 'reference' else 'oracle C port'}"
-            f" run_pipeline with workers={cores} at NM budgets {b1} and {b2}; QAOA stage "
-            f"extrapolated linearly to budget {w['budget']} ({qaoa_full:.2f} s), merge "
-            f"{merge_s:.2f} s measured, total {total:.2f} s per solve of {M} subgraphs")
-    return value, desc, kind, cores, time.time() - t0, total
+    cap26 = w["qubit_cap"] > 24
+    if ref_available(cap26):
+        return RefLib(cap26=cap26), "reference"
+    lib = OracleLib()
+    lib.set_qubit_cap(26 if cap26 else 24)
+    return lib, "port"
+
+
+def reference_full(w, edges, cores):
+    """One full solve of the workload by the reference's stock run_pipeline
+    (pipeline.hpp:391: partition -> QAOA stage -> merge; workers = all host threads)."""
+    lib, kind = ref_lib(w)
+    r = lib.run_pipeline(w["n"], edges, qubit_cap=w["qubit_cap"], top_k=w["top_k"],
+                         layers=w["layers"], budget=w["budget"], seed=w["seed"], workers=cores)
+    value = r["subgraphs"] * w["budget"] / r["total_s"]
+    return value, r, kind
+
+
+def sample_indices(M, S):
+    return sorted(set(int(round(x)) for x in np.linspace(0, M - 1, S)))
+
+
+def reference_sampled(w, edges, cores, indices=None):
+    """A bounded sample of the reference QAOA stage: S = min(cores, M) subgraphs spread over
+    the chain solved concurrently exactly as pipeline.hpp:223-280 schedules one round
+    (slots = min(workers, M) std::threads, threads_per = workers / slots OpenMP threads each,
+    seed = base + idx), at a reduced NM budget b. The stage at the full budget B is then
+    ceil(M/S) such rounds of B/b times the sampled round (the fixed per-solve costs —
+    cost table, final circuit, top-K — are counted B/b times, which overstates the CPU
+    time by at most a few percent; the merge is not included)."""
+    lib, kind = ref_lib(w)
+    M = subgraph_count(w)
+    S = min(cores, M)
+    idx = indices if indices is not None else sample_indices(M, S)
+    b = SAMPLE_BUDGET[w["key"]]
+    threads = max(1, cores // min(S, M))
+    out, secs = lib.solve_stage(w["n"], edges, M, idx, w["top_k"], w["layers"], b,
+                                seed=w["seed"], slots=len(idx), threads=threads,
+                                qubit_cap=w["qubit_cap"])
+    rounds = -(-M // S)
+    stage_s = rounds * secs * (w["budget"] / b)
+    value = M * w["budget"] / stage_s
+    desc = (f"{'oracle/_ref (unmodified qcut headers)' if kind == 'reference' else 'oracle C port'}:"
+            f" {len(idx)} of {M} subgraphs (indices {idx[0]}..{idx[-1]}) solved concurrently "
+            f"({threads} OpenMP thread(s) each, pipeline.hpp:223-280 round) at NM budget {b} in "
+            f"{secs:.2f} s; QAOA stage at budget {w['budget']} = {rounds} rounds x "
+            f"{w['budget'] // b if w['budget'] % b == 0 else w['budget'] / b} x sample = "
+            f"{stage_s:.1f} s (extrapolated; merge excluded)")
+    return value, desc, kind, out, idx, b, secs
+
+
+def cpu_eval_microbench(cores, qs=(10, 16, 20, 24, 26)):
+    """BASELINE.md section 3 step 3 / SURVEY 8(d): seconds per objective evaluation of
+    the reference (run_ansatz + expectation, qaoa.hpp:89-91) at p=1 on ER(q, 0.5) subgraphs,
+    1 and all host threads."""
+    from oracle.refpy import RefLib, ref_available
+    if not ref_available(True):
+        return None
+    lib = RefLib(cap26=True)
+    out = []
+    for q in qs:
+        e = lib.generate_er(q, 0.5, q)
+        for th in sorted({1, cores}):
+            reps = 3 if q <= 20 else 1
+            sec, _ = lib.eval_timing(q, e, [0.4], [0.9], threads=th, reps=reps)
+            out.append({"q": q, "threads": th, "s_per_eval": sec,
+                        "amp_layers_per_s": (1 << q) / sec})
+    return out
 
 
 def run_reference_arm(args, w):
+    """The reference's own CPU implementation on this host, all host threads: C1/C2 are
+    full-budget solves by the stock run_pipeline, timed per step; C3-C5 are the sampled
+    stage of reference_sampled. A wall-clock guard keeps the run inside the driver's
+    step limit: steps stop early (and "steps" says how many ran) past --ref-time-limit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    cores = os.cpu_count() or 1
     edges = workload_graph(w, reference=True)
+    full = w["key"] in FULL_REFERENCE
+    t_start = time.time()
+
+    def step():
+        if full:
+            v, r, kind = reference_full(w, edges, cores)
+            return v, r["total_s"], kind, (f"stock run_pipeline (pipeline.hpp:391) at the full NM "
+                                            f"budget {w['budget']}, workers={cores}: partition "
+                                            f"{r['partition_s']:.3f} s + QAOA {r['qaoa_s']:.2f} s + "
+                                            f"merge {r['merge_s']:.2f} s, cut {r['cut']:.0f}"), r
+        v, desc, kind, _, _, _, _ = reference_sampled(w, edges, cores)
+        return v, subgraph_count(w) * w["budget"] / v, kind, desc, None
+
+    warm_done = 0
     for _ in range(args.warmup):
-        reference_sample(w, edges)
-    vals, totals = [], []
-    desc = kind = cores = None
+        if time.time() - t_start > args.ref_time_limit / 3:
+            break
+        step()
+        warm_done += 1
+    vals, totals, desc, kind, last = [], [], None, None, None
     for _ in range(args.steps):
-        v, desc, kind, cores, _, total = reference_sample(w, edges)
+        el = time.time() - t_start
+        per = (el / max(1, warm_done + len(vals)))
+        if vals and el + per > args.ref_time_limit:
+            break
+        v, total, kind, desc, last = step()
         vals.append(v)
         totals.append(total)
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(vals), "warmup": warm_done,
+        "steps_requested": args.steps, "warmup_requested": args.warmup,
         "ms_per_step": statistics.median(totals) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
-                   "qubit_cap": w["qubit_cap"], "layers": w["layers"], "top_k": w["top_k"],
-                   "budget": w["budget"], "parallelism": f"cpu x{cores} threads"},
+        "config": config_dict(w, args.gpus),
+        "measured": "full solve per step" if full else "sampled stage, extrapolated",
+        "extrapolated": not full,
+        "step_s": [round(t, 3) for t in totals],
+        "wall_s": round(time.time() - t_start, 1),
+        "host": host_info(),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if last is not None:
+        line["result"] = {"cut": last["cut"], "candidates_evaluated": last["leaves"],
+                          "assignment_sha1": __import__("hashlib").sha1(
+                              last["assignment"].encode()).hexdigest()}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def parity_full(w, edges, cores, rep, records):
+    """cpu_baseline for C1/C2 plus the parity block: the reference's stock run_pipeline at
+    the full budget (timed -> cpu_baseline) and every SolveResult of its QAOA stage
+    (ref_solve_stage) against the GPU's timed run (the cut, assignment, leaves of the last
+    timed step; the SolveResults of the resident session, qc_pipeline_records)."""
+    value, r, kind = reference_full(w, edges, cores)
+    lib, _ = ref_lib(w)
+    M = r["subgraphs"]
+    want, _ = lib.solve_stage(w["n"], edges, M, list(range(M)), w["top_k"], w["layers"],
+                              w["budget"], seed=w["seed"], slots=min(cores, M), threads=1,
+                              qubit_cap=w["qubit_cap"])
+    L = w["layers"]
+    same = [bool(g.width == o.width and np.array_equal(g.bits, o.bits) and
+                 np.array_equal(g.probs, o.probs) and np.array_equal(g.params[:2 * L], o.params[:2 * L])
+                 and g.expectation == o.expectation and g.evals == o.evals)
+            for g, o in zip(records, want)]
+    parity = {
+        "checker": "oracle/_ref stock run_pipeline + ref_solve_stage" if kind == "reference"
+        else "oracle C port",
+        "budget": w["budget"], "subgraphs": M,
+        "cut": [rep.cut, r["cut"]], "cut_equal": rep.cut == r["cut"],
+        "assignment_equal": rep.assignment == r["assignment"],
+        "candidates_evaluated_equal": rep.candidates_evaluated == r["leaves"],
+        "expectations_equal": [x.expectation for x in records] == list(r["sub_expectation"]),
+        "evals_equal": [x.evals for x in records] == list(r["sub_evals"]),
+        "solve_results_equal": sum(same), "solve_results_compared": len(same),
+    }
+    parity["all_equal"] = bool(parity["cut_equal"] and parity["assignment_equal"] and
+                               parity["candidates_evaluated_equal"] and parity["expectations_equal"]
+                               and parity["evals_equal"] and all(same) and len(same) == M)
+    desc = (f"{'oracle/_ref (unmodified qcut headers)' if kind == 'reference' else 'oracle C port'}"
+            f" stock run_pipeline, one full solve at NM budget {w['budget']}, workers={cores}: "
+            f"partition {r['partition_s']:.3f} s + QAOA {r['qaoa_s']:.2f} s + merge "
+            f"{r['merge_s']:.2f} s = {r['total_s']:.2f} s")
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}, parity
+
+
+def parity_sampled(eng, w, edges, cores):
+    """cpu_baseline for C3-C5 (reference_sampled) plus the parity block: the same sampled
+    subgraphs solved by the product at the sample budget, every SolveResult identical."""
+    from paper_2603_26232_b200 import partition_chain
+    value, desc, kind, want, idx, b, _ = reference_sampled(w, edges, cores)
+    P = partition_chain(w["n"], edges, subgraph_count(w), 0, w["qubit_cap"])
+    graphs, opts = [], []
+    for i in idx:
+        nl, le = P.local[i]
+        k = min(1 << (nl - 1), w["top_k"]) if w["top_k"] else 1 << (nl - 1)
+        graphs.append((nl, le))
+        opts.append(dict(top_k=k, layers=w["layers"], budget=b, seed=w["seed"] + i,
+                         qubit_cap=w["qubit_cap"]))
+    got = eng.solve_batch(graphs, opts)
+    L = w["layers"]
+    same = [bool(g.width == o.width and np.array_equal(g.bits, o.bits) and
+                 np.array_equal(g.probs, o.probs) and np.array_equal(g.params[:2 * L], o.params[:2 * L])
+                 and g.expectation == o.expectation and g.evals == o.evals)
+            for g, o in zip(got, want)]
+    parity = {"checker": "oracle/_ref ref_solve_stage" if kind == "reference" else "oracle C port",
+              "sampled_subgraphs": idx, "budget": b, "solve_results_equal": sum(same),
+              "solve_results_compared": len(same), "all_equal": all(same) and len(same) == len(idx),
+              "note": "full-budget sampled solves of this workload: tests/test_gpu_configs.py"}
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": desc}, parity
 
 
 # --------------------------------------------------------------------------------------
@@ -271,8 +452,13 @@ def main():
                          "'gpu' section to this path")
     ap.add_argument("--profile-stride", type=int, default=PROFILE_STRIDE,
                     help="CUDA-event sampling of 1 launch in N during the timed region (0: off)")
+    ap.add_argument("--ref-time-limit", type=float, default=1500.0,
+                    help="reference arm: stop starting steps past this many seconds")
+    ap.add_argument("--no-cpu-microbench", action="store_true",
+                    help="skip the per-eval CPU microbenchmark of the cpu_baseline leg")
     args = ap.parse_args()
     w = dict(WORKLOADS[args.workload])
+    w["key"] = args.workload
     if args.impl == "reference":
         return run_reference_arm(args, w)
 
@@ -309,6 +495,7 @@ def main():
         torch.cuda.synchronize()
 
     # ---- single GPU: resident session (value) -------------------------------------
+    sess = None
     if world == 1:
         sess = eng.prepare_pipeline(w["n"], edges, **cfg)
         M = None
@@ -423,11 +610,13 @@ def main():
     iso_ms = sum(v["ms"] for v in profile_iso.values())
     iso_bytes = sum(v["bytes"] for v in profile_iso.values())
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
-    traffic = None
-    try:
+    fp_tag = "f64" if args.precision == 64 else "f32"
+    traffic, traffic_src = None, None
+    try:  # ncu DRAM bytes per launch of THIS workload's dominant kernel (tools/ncu_traffic.py)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(dom)
-            traffic = tr.get("dram_bytes_per_launch") if tr else None
+            tr = json.load(f).get(f"{w['key']}/{fp_tag}/{dom}")
+        if tr:
+            traffic, traffic_src = tr.get("dram_bytes_per_launch"), tr.get("source")
     except Exception:
         pass
     fp64_peak = FP64_PEAK_TOPS
@@ -440,39 +629,59 @@ def main():
                 ss["frac"] = ss["achieved"] / peak
         except Exception as ex:  # diagnostic only: never fail the bench on it
             ss = {"error": str(ex)[:200]}
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind ==
-                "measured" else "fallback (B200_PROFILING.md)",
-                "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
-                "avg_launch_ms": d["ms"] / max(d["launches"], 1),
-                "measured": "every launch of one single-stream step, CUDA events on its stream",
-                "launches": d["launches"],
-                "share_of_step": d["ms"] / iso_ms if iso_ms else None,
-                # streaming efficiency without the per-launch fixed cost (see steady_state)
-                "steady_state": ss,
-                # the fp64 parity path forbids FMA: every butterfly is 8 DMUL + 4 DADD, so
-                # the FP64 pipe is the second ceiling (co-bound for the 12-target pass A)
-                "fp64": {"achieved_tops": fp64_ach, "peak_tops": fp64_peak,
-                         "frac": fp64_ach / fp64_peak,
-                         "ops_per_launch": d.get("fp64_ops", 0.0) / max(d["launches"], 1),
-                         "peak_source": "measured: tools/ubench_fp64.cu mixer_pair pattern "
-                                        "(profiles/r1_ubench_fp64.txt)"},
-                "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                                "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
-                                if v["ms"] > 0 else 0.0,
-                                "fp64_Tops": round(v.get("fp64_ops", 0.0) / (v["ms"] / 1e3) / 1e12, 2)
-                                if v["ms"] > 0 else 0.0}
-                            for k, v in profile_iso.items() if v["launches"]},
-                # all engine kernels' algorithmic bytes of one step / timed step time
-                "step_aggregate_GBs": iso_bytes / sec_per_step / 1e9,
-                "step_aggregate_frac": iso_bytes / sec_per_step / 1e9 / peak,
-                "timed_region_sampled": {
-                    "stride": args.profile_stride, "streams": 2,
-                    "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
-                                    "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
-                                    if v["ms"] > 0 else 0.0}
-                                for k, v in profile.items() if v["launches"]}}}
+    kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                   "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1) if v["ms"] > 0 else 0.0,
+                   "fp64_Tops": round(v.get("fp64_ops", 0.0) / (v["ms"] / 1e3) / 1e12, 2)
+                   if v["ms"] > 0 else 0.0}
+               for k, v in profile_iso.items() if v["launches"]}
+    common = {"kernel": dom, "avg_launch_ms": d["ms"] / max(d["launches"], 1),
+              "measured": "every launch of one single-stream step, CUDA events on its stream",
+              "launches": d["launches"], "share_of_step": d["ms"] / iso_ms if iso_ms else None,
+              "kernels": kernels,
+              "step_aggregate_GBs": iso_bytes / sec_per_step / 1e9,
+              "step_aggregate_frac": iso_bytes / sec_per_step / 1e9 / peak,
+              "timed_region_sampled": {
+                  "stride": args.profile_stride, "streams": 2,
+                  "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                                  "GB/s": round(v["bytes"] / (v["ms"] / 1e3) / 1e9, 1)
+                                  if v["ms"] > 0 else 0.0}
+                              for k, v in profile.items() if v["launches"]}}}
+    if dom == "onchip":
+        # whole subgraph state in one CTA's shared memory for every layer: no HBM stream,
+        # the ceiling is the FP64 pipe (explicit DMUL/DADD, no FMA) — and dependent latency
+        roofline = {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak, "unit": "Tops/s",
+                    "frac": fp64_ach / fp64_peak, "traffic": traffic,
+                    "peak_source": "measured: tools/ubench_fp64.cu mixer_pair pattern "
+                                   "(profiles/r1_ubench_fp64.txt)",
+                    "algorithmic_fp64_ops_per_launch": d.get("fp64_ops", 0.0) / max(d["launches"], 1),
+                    "note": "on-chip kernel (Q <= 12): HBM is not touched between layers, so an HBM "
+                            "fraction is meaningless; FP64 issue and latency bound it", **common}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind ==
+                    "measured" else "fallback (B200_PROFILING.md)",
+                    "algorithmic_bytes_per_launch": d["bytes"] / max(d["launches"], 1),
+                    # streaming efficiency without the per-launch fixed cost (see steady_state)
+                    "steady_state": ss,
+                    # the fp64 parity path forbids FMA: every butterfly is 8 DMUL + 4 DADD, so
+                    # the FP64 pipe is the second ceiling (co-bound for the 12-target pass A)
+                    "fp64": {"achieved_tops": fp64_ach, "peak_tops": fp64_peak,
+                             "frac": fp64_ach / fp64_peak,
+                             "ops_per_launch": d.get("fp64_ops", 0.0) / max(d["launches"], 1),
+                             "peak_source": "measured: tools/ubench_fp64.cu mixer_pair pattern "
+                                            "(profiles/r1_ubench_fp64.txt)"},
+                    **common}
+    q = w["qubit_cap"]
+    amp_b = 16 if args.precision == 64 else 8
+    ws = subgraph_count(w) * (1 << (q - 1)) * (amp_b + amp_b // 2)
+    l2 = (f"per-step working set {ws / 2**20:.0f} MiB (states + f of {subgraph_count(w)} "
+          f"half-states of {q} qubits) {'>' if ws > 126 * 2**20 else '<'} 126 MB L2; "
+          f"L2 flushed (256 MB write) before every timed step")
+    if dom == "onchip":
+        l2 = (f"on-chip kernel: each {q}-qubit state lives in shared memory for the whole eval; "
+              f"inputs ({ws / 2**10:.0f} KiB) come from L2; L2 flushed (256 MB write) before "
+              f"every timed step")
 
     line = {
         "metric": METRIC, "value": evals_per_step / sec_per_step, "unit": UNIT,
@@ -480,11 +689,7 @@ def main():
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
         "data": "synthetic (graph.hpp:146 ER generator restated in qc_generate_er)",
-        "config": {"workload": w["label"], "n": w["n"], "p_edge": w.get("p_edge"),
-                   "qubit_cap": w["qubit_cap"], "subgraphs": n_sub, "layers": w["layers"],
-                   "top_k": w["top_k"], "budget": w["budget"], "parallelism": f"shard{world}",
-                   "l2": "working set (21 half-states x 8 MiB + f buffers) > 126 MB L2; "
-                         "L2 flushed (256 MB write) between timed steps"},
+        "config": config_dict(w, world), "l2": l2,
         "solve_time_s": sec_per_step, "cut": rep.cut, "evals_per_step": evals_per_step,
         "step_ms": [round(t * 1e3, 2) for t in t_val],
         "host_s_per_step": {k: (v / args.steps if k != "chunk_steps" else v // args.steps)
@@ -493,13 +698,23 @@ def main():
         "e2e": e2e, "gpu_launches": int(lt.item()), "clocks": clk, "roofline": roofline,
     }
     if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
         try:
-            v, desc, kind, cores, _, total = reference_sample(w, workload_graph(w, reference=True))
-            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                                    "sample": desc}
+            ref_edges = workload_graph(w, reference=True)
+            if w["key"] in FULL_REFERENCE:
+                cb, parity = parity_full(w, ref_edges, cores, rep, sess.records())
+            else:
+                cb, parity = parity_sampled(eng, w, ref_edges, cores)
+            line["cpu_baseline"], line["parity"] = cb, parity
         except Exception as ex:  # report, never fail the bench line
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
-                                    "kind": "unavailable", "sample": str(ex)}
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cores,
+                                    "kind": "unavailable", "sample": repr(ex)[:300]}
+        line["cpu_baseline"]["host"] = host_info()
+        if not args.no_cpu_microbench and w["key"] == "c2":
+            try:
+                line["cpu_baseline"]["per_eval"] = cpu_eval_microbench(cores)
+            except Exception as ex:
+                line["cpu_baseline"]["per_eval"] = repr(ex)[:200]
     print(json.dumps(line), flush=True)
     if args.report and rep is not None:
         from paper_2603_26232_b200.report import emit_report, experiment_report
@@ -509,8 +724,9 @@ def main():
             gpu={"device": torch.cuda.get_device_name(local), "n_gpus": world,
                  "precision": f"fp{args.precision}", "evals_per_s": line["value"],
                  "e2e_evals_per_s": e2e["value"], "ms_per_step": line["ms_per_step"],
-                 "roofline": {"kernel": roofline["kernel"], "hbm_frac": roofline["frac"],
-                              "fp64_frac": roofline["fp64"]["frac"]},
+                 "roofline": {"kernel": roofline["kernel"], "bound": roofline["bound"],
+                              "frac": roofline["frac"],
+                              "fp64_frac": roofline.get("fp64", roofline)["frac"]},
                  "clocks": clk})
         with open(args.report, "w") as f:
             f.write(emit_report(doc))

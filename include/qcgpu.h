@@ -39,7 +39,7 @@ extern "C" {
 #define QC_ERR_IO 3
 #define QC_ERR_INTERNAL 4
 
-#define QC_ABI_VERSION 1
+#define QC_ABI_VERSION 2
 
 typedef struct qc_engine qc_engine;
 
@@ -284,10 +284,10 @@ int qc_chained_merge(qc_engine* e, const qc_pool* pool, const qc_graph* g,
 /* ---- pipeline.hpp (hot-path stages) ------------------------------------------- */
 /* pipeline.hpp:111-124 schedule rounds are replaced by one batched solve; this runs
  * partition (partition.hpp:111) -> QAOA stage (pipeline.hpp:219-296) -> merge
- * (pipeline.hpp:298-334) for graph g and fills report + assignment (n bytes '0'/'1'
- * plus NUL). With shard_count > 1 only the QAOA stage of shard shard_index runs and
- * qc_run_pipeline returns after writing the shard's solve records (see
- * qc_shard_solve); the merge then runs on the gathered records (qc_merge_records). */
+ * (pipeline.hpp:298-334) for graph g on one GPU and fills report + assignment (n bytes
+ * '0'/'1' plus NUL). cfg->shard_count must be 1: multi-GPU callers use
+ * qc_run_pipeline_multi (one process, n GPUs) or, one process per GPU,
+ * qc_shard_solve -> qc_gather_topk -> qc_merge_records. */
 int qc_run_pipeline(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
                     qc_run_report* report, char* assignment);
 
@@ -300,16 +300,59 @@ int qc_pipeline_prepare(qc_engine* e, const qc_graph* g, const qc_run_config* cf
 int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment);
 void qc_pipeline_destroy(qc_pipeline* pl);
 
-/* Multi-GPU: fixed-size solve records for the NCCL gather.
- * record_bytes(top_k_cap, layers) gives the size of one record; qc_shard_solve solves
- * subgraphs [begin, end) of the partition of g and writes end-begin records;
- * qc_merge_records merges M records (all shards, in subgraph order). */
+/* SolveResults of the last qc_pipeline_execute as solve records (layout below), in
+ * subgraph order; with records == NULL only *record_bytes / *subgraphs are written. */
+int qc_pipeline_records(const qc_pipeline* pl, void* records, int64_t capacity,
+                        int64_t* record_bytes, int32_t* subgraphs);
+
+/* ---- multi-GPU: shards of subgraphs, one gather of solve records ----
+ * Solve record (fixed size per run, qc_run_record_bytes): int32 {width, count, evals,
+ * folded}, double expectation, uint32 bits[kcap] (padded to 8 bytes), double probs[kcap],
+ * double params[2*layers] — one SolveResult (qaoa.hpp:147-152) of pipeline.hpp:263.
+ * kcap = min(top_k, classes of the widest piece), or every class for top_k = 0. */
 int64_t qc_record_bytes(int top_k_cap, int layers);
+/* Record size and subgraph count of the run (g, cfg): the geometry every rank and the
+ * merge must agree on (derived from the same chain partition as qc_shard_solve). */
+int qc_run_record_bytes(const qc_graph* g, const qc_run_config* cfg, int64_t* record_bytes,
+                        int32_t* subgraphs);
+/* Contiguous balanced block [begin, end) of the M subgraphs for shard shard_index. */
 int qc_shard_range(int M, int shard_index, int shard_count, int32_t* begin, int32_t* end);
+/* pipeline.hpp:239-263 for subgraphs [begin, end) of g's partition on this engine:
+ * writes end-begin records (capacity: bytes of `records`; config error if short). With
+ * records == NULL only *subgraphs (= M) is written. */
 int qc_shard_solve(qc_engine* e, const qc_graph* g, const qc_run_config* cfg, int32_t begin,
-                   int32_t end, void* records, int32_t* subgraphs);
+                   int32_t end, void* records, int64_t capacity, int32_t* subgraphs);
+/* pipeline.hpp:298-334 on the M gathered records (all shards, subgraph order). */
 int qc_merge_records(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
-                     const void* records, int32_t M, qc_run_report* report, char* assignment);
+                     const void* records, int64_t capacity, int32_t M, qc_run_report* report,
+                     char* assignment);
+
+/* NCCL record gather (replaces the hand-over of SolveResults from the per-subgraph
+ * threads of pipeline.hpp:271-280 to the merge at pipeline.hpp:300-305). One rank per
+ * GPU: rank 0 calls qc_comm_id, the caller ships the 128 bytes to every rank (MPI, a
+ * file, torch.distributed, ...), each rank calls qc_comm_create on its engine. One
+ * process driving several GPUs: qc_comm_create_all (ncclCommInitAll; one engine per
+ * distinct device) fills out[n]. NCCL is loaded at first use (libnccl.so.2). */
+#define QC_COMM_ID_BYTES 128
+typedef struct qc_comm qc_comm;
+int qc_comm_id(void* id /* QC_COMM_ID_BYTES */);
+int qc_comm_create(qc_engine* e, int nranks, int rank, const void* id, qc_comm** out);
+int qc_comm_create_all(qc_engine* const* engines, int n, qc_comm** out);
+int qc_comm_rank(const qc_comm* c, int32_t* rank, int32_t* nranks);
+void qc_comm_destroy(qc_comm* c);
+/* All-gather of solve records over NCCL on the engine's stream: this rank holds the
+ * `count` records of its qc_shard_range block; `all` receives the M records of every
+ * rank in subgraph order (M * record_bytes bytes). Collective: every rank calls it. */
+int qc_gather_topk(qc_comm* c, const void* local, int32_t count, int32_t M, int64_t record_bytes,
+                   void* all);
+/* One process, n engines: shard -> per-engine solve (one host thread each) -> record
+ * all-gather over comms (NCCL; comms[i] = rank i on engines[i], from
+ * qc_comm_create_all) -> merge on engines[0]. comms == NULL (engines that share a
+ * device, where NCCL cannot form a communicator): the records are concatenated in host
+ * memory instead. Same results as qc_run_pipeline. */
+int qc_run_pipeline_multi(qc_engine* const* engines, qc_comm* const* comms, int n,
+                          const qc_graph* g, const qc_run_config* cfg, qc_run_report* report,
+                          char* assignment);
 
 #ifdef __cplusplus
 }

@@ -442,21 +442,29 @@ int ref_run_pipeline(int n, int m, const RefEdge* e, const RefRunConfig* c, RefR
     });
 }
 
-// Solve a contiguous set of pipeline subgraphs exactly as the QAOA stage does
-// (pipeline.hpp:239-263: seed = base + idx, top_k clamp), `threads` OpenMP
-// threads each, `slots` concurrent std::threads. Returns wall seconds. Used by
-// bench.py's reference arm as a bounded sample of the stage.
-int ref_qaoa_stage_sample(int n, int m, const RefEdge* e, int M, int first_idx, int count,
-                          int top_k, int layers, int budget, std::uint64_t seed, int fold,
-                          int slots, int threads, int qubit_cap, double tol, double* seconds) {
+// The QAOA stage of pipeline.hpp:219-296 for a chosen list of subgraph indices: the
+// reference's own partition (partition.hpp:111), the stage's per-index SolveOptions
+// (seed = base + idx, top_k clamp, pipeline.hpp:245-261) and its concurrency (`slots`
+// std::threads per round, `threads` OpenMP threads each, pipeline.hpp:223-227). Every
+// SolveResult is written out: widths/counts[count], bits/probs[count][kcap],
+// params[count][2*layers] (gammas then betas), expect/evals[count]. seconds = wall time
+// of the solves. Used by the GPU parity tests (full-budget solves of sampled subgraphs
+// at configs 3-5) and by bench.py's parity block.
+int ref_solve_stage(int n, int m, const RefEdge* e, int M, int mode, int qubit_cap,
+                    const int* idx, int count, int top_k, int layers, int budget,
+                    std::uint64_t seed, int fold, int slots, int threads, double tol, int kcap,
+                    int* widths, int* counts, std::uint32_t* bits, double* probs, double* params,
+                    double* expect, int* evals, double* seconds) {
     return guarded([&] {
         const auto g = make_graph(n, m, e);
-        const auto part = make_partition(g, M, 0, qubit_cap);
+        const auto part = make_partition(g, M, mode, qubit_cap);
         std::vector<std::exception_ptr> errs(static_cast<std::size_t>(count));
         auto solve_one = [&](int k) {
             try {
-                const int idx = first_idx + k;
-                const auto& sub = part.subgraphs[static_cast<std::size_t>(idx)];
+                const int id = idx[k];
+                if (id < 0 || id >= static_cast<int>(part.subgraphs.size()))
+                    throw qcut::config_error("subgraph index out of range");
+                const auto& sub = part.subgraphs[static_cast<std::size_t>(id)];
                 const std::size_t classes = fold ? (std::size_t{1} << (sub.size() - 1))
                                                  : (std::size_t{1} << sub.size());
                 qcut::SolveOptions so;
@@ -465,12 +473,26 @@ int ref_qaoa_stage_sample(int n, int m, const RefEdge* e, int M, int first_idx, 
                                             classes, static_cast<std::size_t>(top_k)));
                 so.layers = layers;
                 so.budget = budget;
-                so.seed = seed + static_cast<std::uint64_t>(idx);
+                so.seed = seed + static_cast<std::uint64_t>(id);
                 so.fold = fold != 0;
                 so.threads = threads;
                 so.qubit_cap = static_cast<std::size_t>(qubit_cap);
                 so.tolerance = tol;
-                (void)qcut::solve_subgraph(sub.local_graph, so);
+                if (so.top_k > kcap) throw qcut::config_error("kcap below the retained count");
+                const auto r = qcut::solve_subgraph(sub.local_graph, so);
+                const auto kk = static_cast<std::size_t>(k);
+                widths[kk] = static_cast<int>(r.candidates.width);
+                counts[kk] = static_cast<int>(r.candidates.entries.size());
+                for (std::size_t i = 0; i < r.candidates.entries.size(); ++i) {
+                    bits[kk * static_cast<std::size_t>(kcap) + i] = r.candidates.entries[i].bits;
+                    probs[kk * static_cast<std::size_t>(kcap) + i] = r.candidates.entries[i].probability;
+                }
+                for (int l = 0; l < layers; ++l) {
+                    params[kk * 2 * static_cast<std::size_t>(layers) + static_cast<std::size_t>(l)] = r.params.gammas[static_cast<std::size_t>(l)];
+                    params[kk * 2 * static_cast<std::size_t>(layers) + static_cast<std::size_t>(layers + l)] = r.params.betas[static_cast<std::size_t>(l)];
+                }
+                expect[kk] = r.expectation;
+                evals[kk] = r.evals;
             } catch (...) {
                 errs[static_cast<std::size_t>(k)] = std::current_exception();
             }
@@ -484,6 +506,27 @@ int ref_qaoa_stage_sample(int n, int m, const RefEdge* e, int M, int first_idx, 
         *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         for (auto& x : errs)
             if (x) std::rethrow_exception(x);
+    });
+}
+
+// Per-eval CPU baseline: the objective of optimize_parameters
+// (qaoa.hpp:89-91: run_ansatz + expectation on a prebuilt CostTable) evaluated `reps`
+// times at fixed angles with `threads` OpenMP threads. Writes seconds per evaluation and
+// the last expectation (so the loop cannot be elided).
+int ref_eval_timing(int n, int m, const RefEdge* e, int p, const double* gammas,
+                    const double* betas, int threads, int reps, double* sec_per_eval,
+                    double* expect) {
+    return guarded([&] {
+        const auto g = make_graph(n, m, e);
+        const qcut::CostTable table(g, qcut::kQubitCap);
+        const auto params = make_params(p, gammas, betas);
+        double x = 0.0;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < reps; ++r)
+            x = qcut::expectation(qcut::run_ansatz(table, params, threads), table, threads);
+        *sec_per_eval = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() /
+                        static_cast<double>(reps > 0 ? reps : 1);
+        *expect = x;
     });
 }
 

@@ -88,6 +88,7 @@ class SolveOut:
     params: np.ndarray
     expectation: float
     evals: int
+    width: int = 0
 
 
 @dataclass
@@ -309,15 +310,81 @@ class RefLib(_Lib):
     def qubit_cap(self) -> int:
         return self.lib.ref_qubit_cap()
 
-    def qaoa_stage_sample(self, n, edges, M, first_idx, count, top_k, layers, budget, seed,
-                          fold, slots, threads, qubit_cap, tol=1e-5) -> float:
+    def solve_stage(self, n, edges, M, indices, top_k, layers, budget, seed=0, fold=True,
+                    slots=1, threads=1, qubit_cap=20, tol=1e-5, mode=0):
+        """pipeline.hpp:219-296's QAOA stage for the subgraphs `indices` of the reference's
+        own partition (ref_solve_stage): one SolveOut per index, plus wall seconds."""
         e = edges_array(edges)
+        idx = np.ascontiguousarray(indices, np.int32)
+        cnt = len(idx)
+        kcap = max(int(top_k), 1) if top_k else (1 << (qubit_cap - 1 if fold else qubit_cap))
+        widths = np.zeros(cnt, np.int32)
+        counts = np.zeros(cnt, np.int32)
+        bits = np.zeros((cnt, kcap), np.uint32)
+        probs = np.zeros((cnt, kcap))
+        params = np.zeros((cnt, 2 * layers))
+        ex = np.zeros(cnt)
+        ev = np.zeros(cnt, np.int32)
         secs = C.c_double(0)
-        self._call("qaoa_stage_sample", C.c_int(n), C.c_int(len(e)), _p(e), C.c_int(M),
-                   C.c_int(first_idx), C.c_int(count), C.c_int(top_k), C.c_int(layers),
+        self._call("solve_stage", C.c_int(n), C.c_int(len(e)), _p(e), C.c_int(M), C.c_int(mode),
+                   C.c_int(qubit_cap), _p(idx), C.c_int(cnt), C.c_int(top_k), C.c_int(layers),
                    C.c_int(budget), C.c_uint64(seed), C.c_int(int(fold)), C.c_int(slots),
-                   C.c_int(threads), C.c_int(qubit_cap), C.c_double(tol), C.byref(secs))
-        return secs.value
+                   C.c_int(threads), C.c_double(tol), C.c_int(kcap), _p(widths), _p(counts),
+                   _p(bits), _p(probs), _p(params), _p(ex), _p(ev), C.byref(secs))
+        out = [SolveOut(bits[k, : counts[k]].copy(), probs[k, : counts[k]].copy(), params[k].copy(),
+                        float(ex[k]), int(ev[k])) for k in range(cnt)]
+        for o, w in zip(out, widths):
+            o.width = int(w)
+        return out, secs.value
+
+    def eval_timing(self, n, edges, gammas, betas, threads=1, reps=3):
+        """Seconds per objective evaluation (run_ansatz + expectation on a prebuilt
+        CostTable, qaoa.hpp:89-91) at fixed angles, and the expectation."""
+        e = edges_array(edges)
+        g = np.ascontiguousarray(gammas, np.float64)
+        b = np.ascontiguousarray(betas, np.float64)
+        sec = C.c_double(0)
+        ex = C.c_double(0)
+        self._call("eval_timing", C.c_int(n), C.c_int(len(e)), _p(e), C.c_int(len(g)), _p(g),
+                   _p(b), C.c_int(threads), C.c_int(reps), C.byref(sec), C.byref(ex))
+        return sec.value, ex.value
+
+
+class RefChecker:
+    """The parity checker of the -m gpu tests: the reference build itself (RefLib over
+    oracle/_ref/libqcut_ref.so; libqcut_ref26.so once set_qubit_cap(26), BASELINE config 5),
+    with the C restatement (OracleLib) only for what the reference has no function for
+    (the config-3 regular generator). Same Python surface as OracleLib."""
+
+    kind = "reference"
+
+    def __init__(self):
+        self._r24 = RefLib()
+        self._r26 = RefLib(cap26=True) if ref_available(True) else None
+        self._cur = self._r24
+        self._orc = OracleLib() if oracle_available() else None
+
+    def set_qubit_cap(self, cap: int):
+        if cap > 24 and self._r26 is None:
+            raise FileNotFoundError(REF26_SO)
+        self._cur = self._r26 if cap > 24 else self._r24
+
+    def qubit_cap(self) -> int:
+        return self._cur.qubit_cap()
+
+    def generate_regular(self, *a, **kw):
+        return self._orc.generate_regular(*a, **kw)
+
+    def __getattr__(self, name):
+        return getattr(self._cur, name)
+
+
+def checker():
+    """RefChecker when oracle/_ref was built (this container; the .so files travel to the
+    GPU box in the repo snapshot), else the C restatement."""
+    if ref_available() and ref_available(True):
+        return RefChecker()
+    return OracleLib()
 
 
 class OracleLib(_Lib):

@@ -21,7 +21,8 @@ import numpy as np
 __all__ = [
     "Engine", "QcError", "ConfigError", "ResourceError", "IoError", "InternalError",
     "EDGE_DTYPE", "edges_array", "library_path", "load_library", "SolveResult", "MergeResult",
-    "RunReport", "Partition", "partition_chain", "derive_subgraph_count",
+    "RunReport", "Partition", "partition_chain", "derive_subgraph_count", "Comm",
+    "run_pipeline_multi", "run_record_bytes", "unpack_records",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -126,6 +127,9 @@ EXPORTED_SYMBOLS = [
     "qc_simplex_result", "qc_simplex_destroy", "qc_optimizer_create", "qc_optimizer_ask",
     "qc_optimizer_tell", "qc_optimizer_result", "qc_optimizer_destroy", "qc_generate_er",
     "qc_generate_regular", "qc_engine_host_stats", "qc_engine_phase_times",
+    "qc_engine_set_precision", "qc_engine_profile_read_fp64", "qc_run_record_bytes",
+    "qc_pipeline_records", "qc_comm_id", "qc_comm_create", "qc_comm_create_all",
+    "qc_comm_rank", "qc_comm_destroy", "qc_gather_topk", "qc_run_pipeline_multi",
 ]
 
 KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
@@ -150,6 +154,7 @@ def load_library(path: str | None = None) -> C.CDLL:
     lib.qc_engine_destroy.restype = None
     lib.qc_engine_stream.restype = C.c_void_p
     lib.qc_pipeline_destroy.restype = None
+    lib.qc_comm_destroy.restype = None
     if path is None:
         _LIB = lib
     return lib
@@ -293,12 +298,15 @@ def partition_chain(n: int, edges, M: int, mode: int = 0, cap: int = 0) -> Parti
     piece = last_piece[u] if len(e) else np.zeros(0, np.int64)
     intra = v <= np.asarray(last, np.int64)[piece] if len(e) else np.zeros(0, bool)
     local = []
+    sel = np.nonzero(intra)[0] if len(e) else np.zeros(0, np.int64)
+    sel = sel[np.argsort(piece[sel], kind="stable")]  # by piece, edge-list order inside
+    bounds = np.searchsorted(piece[sel], np.arange(len(first) + 1))
     for i, (a, b) in enumerate(zip(first, last)):
-        sel = intra & (piece == i)
-        le = np.zeros(int(sel.sum()), EDGE_DTYPE)
-        le["u"] = u[sel] - a
-        le["v"] = v[sel] - a
-        le["w"] = e["w"][sel]
+        s_i = sel[bounds[i]:bounds[i + 1]]
+        le = np.zeros(len(s_i), EDGE_DTYPE)
+        le["u"] = u[s_i] - a
+        le["v"] = v[s_i] - a
+        le["w"] = e["w"][s_i]
         local.append((b - a + 1, le))
     return Partition(np.asarray(first, np.int32), np.asarray(last, np.int32), local,
                      int((~intra).sum()) if len(e) else 0)
@@ -608,17 +616,22 @@ class Engine:
         c = self.run_config(**cfg)
         M = C.c_int32(0)
         self._call("qc_shard_solve", C.byref(g), C.byref(c), C.c_int32(0), C.c_int32(0), None,
-                   C.byref(M))
+                   C.c_int64(0), C.byref(M))
         return M.value
+
+    def run_record_bytes(self, n: int, edges, **cfg) -> tuple[int, int]:
+        """(record bytes, M) of the run: the geometry qc_shard_solve / qc_gather_topk /
+        qc_merge_records use (widest piece of the same chain partition)."""
+        return run_record_bytes(n, edges, **cfg)
 
     def shard_solve(self, n: int, edges, begin: int, end: int, record_bytes: int,
                     **cfg) -> np.ndarray:
         g, ke = _graph(n, edges)
         c = self.run_config(**cfg)
-        buf = np.zeros(max(end - begin, 1) * record_bytes, np.uint8)
+        buf = np.zeros(max((end - begin) * record_bytes, 1), np.uint8)
         M = C.c_int32(0)
         self._call("qc_shard_solve", C.byref(g), C.byref(c), C.c_int32(begin), C.c_int32(end),
-                   _p(buf), C.byref(M))
+                   _p(buf), C.c_int64(buf.size), C.byref(M))
         return buf[: (end - begin) * record_bytes]
 
     def merge_records(self, n: int, edges, records: np.ndarray, M: int, **cfg) -> RunReport:
@@ -627,11 +640,120 @@ class Engine:
         rec = np.ascontiguousarray(records, np.uint8)
         rep = _RunReport()
         asg = C.create_string_buffer(n + 1)
-        self._call("qc_merge_records", C.byref(g), C.byref(c), _p(rec), C.c_int32(M),
-                   C.byref(rep), asg)
+        self._call("qc_merge_records", C.byref(g), C.byref(c), _p(rec), C.c_int64(rec.size),
+                   C.c_int32(M), C.byref(rep), asg)
         return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
                          rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
                          asg.value.decode())
+
+
+def run_record_bytes(n: int, edges, **cfg) -> tuple[int, int]:
+    """qc_run_record_bytes (host only): (record bytes, subgraph count M) of (graph, cfg)."""
+    lib = load_library()
+    g, ke = _graph(n, edges)
+    c = Engine.run_config(**cfg)
+    rb = C.c_int64(0)
+    M = C.c_int32(0)
+    _check(lib, lib.qc_run_record_bytes(C.byref(g), C.byref(c), C.byref(rb), C.byref(M)))
+    return int(rb.value), int(M.value)
+
+
+def unpack_records(records: np.ndarray, M: int, record_bytes: int, layers: int) -> list:
+    """Solve records (include/qcgpu.h layout) -> SolveResult per subgraph."""
+    rec = np.ascontiguousarray(records, np.uint8)[: M * record_bytes].reshape(M, record_bytes)
+    body = record_bytes - 24 - 16 * layers  # = 8*ceil(kcap/2) + 8*kcap, strictly increasing
+    kcap = 0
+    while 8 * ((kcap * 4 + 7) // 8) + 8 * kcap < body:
+        kcap += 1
+    if 8 * ((kcap * 4 + 7) // 8) + 8 * kcap != body:
+        raise ConfigError(f"{record_bytes} bytes is not a record size for {layers} layers")
+    boff = 24
+    poff = boff + 8 * ((kcap * 4 + 7) // 8)
+    aoff = poff + 8 * kcap
+    out = []
+    for r in rec:
+        width, count, evals, folded = (int(x) for x in r[:16].view(np.int32))
+        out.append(SolveResult(width, bool(folded), r[boff:boff + 4 * count].view(np.uint32).copy(),
+                               r[poff:poff + 8 * count].view(np.float64).copy(),
+                               r[aoff:aoff + 16 * layers].view(np.float64).copy(),
+                               float(r[16:24].view(np.float64)[0]), evals))
+    return out
+
+
+class Comm:
+    """qc_comm: one rank of the NCCL record-gather communicator (include/qcgpu.h)."""
+
+    ID_BYTES = 128
+
+    def __init__(self, engine: Engine, handle):
+        self.engine = engine
+        self._h = handle
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = load_library()
+        buf = C.create_string_buffer(Comm.ID_BYTES)
+        _check(lib, lib.qc_comm_id(buf))
+        return buf.raw
+
+    @classmethod
+    def create(cls, engine: Engine, nranks: int, rank: int, uid: bytes) -> "Comm":
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), Comm.ID_BYTES)
+        _check(engine.lib, engine.lib.qc_comm_create(engine._h, C.c_int(nranks), C.c_int(rank),
+                                                     buf, C.byref(h)))
+        return cls(engine, h)
+
+    @classmethod
+    def create_all(cls, engines) -> list:
+        n = len(engines)
+        hs = (C.c_void_p * n)(*[e._h.value for e in engines])
+        out = (C.c_void_p * n)()
+        lib = engines[0].lib
+        _check(lib, lib.qc_comm_create_all(hs, C.c_int(n), out))
+        return [cls(e, C.c_void_p(out[i])) for i, e in enumerate(engines)]
+
+    def rank(self) -> tuple[int, int]:
+        r, nr = C.c_int32(0), C.c_int32(0)
+        _check(self.engine.lib, self.engine.lib.qc_comm_rank(self._h, C.byref(r), C.byref(nr)))
+        return r.value, nr.value
+
+    def gather_topk(self, local: np.ndarray, count: int, M: int, record_bytes: int) -> np.ndarray:
+        loc = np.ascontiguousarray(local, np.uint8)
+        out = np.zeros(max(M * record_bytes, 1), np.uint8)
+        _check(self.engine.lib, self.engine.lib.qc_gather_topk(
+            self._h, _p(loc) if loc.size else None, C.c_int32(count), C.c_int32(M),
+            C.c_int64(record_bytes), _p(out)))
+        return out[: M * record_bytes]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.engine.lib.qc_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_pipeline_multi(engines, n: int, edges, comms=None, **cfg) -> RunReport:
+    """qc_run_pipeline_multi: one process, one engine per GPU; NCCL record gather over
+    `comms` (Comm.create_all), or a host-memory gather when comms is None."""
+    lib = engines[0].lib
+    k = len(engines)
+    hs = (C.c_void_p * k)(*[e._h.value for e in engines])
+    cs = (C.c_void_p * k)(*[c._h.value for c in comms]) if comms else None
+    g, ke = _graph(n, edges)
+    c = Engine.run_config(**cfg)
+    rep = _RunReport()
+    asg = C.create_string_buffer(n + 1)
+    _check(lib, lib.qc_run_pipeline_multi(hs, cs, C.c_int(k), C.byref(g), C.byref(c),
+                                          C.byref(rep), asg))
+    return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
+                     rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
+                     asg.value.decode())
 
 
 class PipelineSession:
@@ -640,6 +762,7 @@ class PipelineSession:
     def __init__(self, engine: Engine, n: int, edges, **cfg):
         self.engine = engine
         self.n = n
+        self.layers = int(cfg.get("layers", 3))
         g, self._edges = _graph(n, edges)
         c = engine.run_config(**cfg)
         h = C.c_void_p()
@@ -654,6 +777,17 @@ class PipelineSession:
         return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
                          rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
                          asg.value.decode())
+
+    def records(self) -> list:
+        """SolveResults of the last execute() (qc_pipeline_records), in subgraph order."""
+        lib = self.engine.lib
+        rb = C.c_int64(0)
+        M = C.c_int32(0)
+        _check(lib, lib.qc_pipeline_records(self._h, None, C.c_int64(0), C.byref(rb), C.byref(M)))
+        buf = np.zeros(max(rb.value * M.value, 1), np.uint8)
+        _check(lib, lib.qc_pipeline_records(self._h, _p(buf), C.c_int64(buf.size), C.byref(rb),
+                                            C.byref(M)))
+        return unpack_records(buf, M.value, rb.value, self.layers)
 
     def close(self):
         if getattr(self, "_h", None):

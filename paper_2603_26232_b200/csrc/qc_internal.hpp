@@ -3,7 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -26,6 +28,37 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
         cudaError_t err_ = (x);                                           \
         if (err_ != cudaSuccess) ::qcg::cuda_fail(err_, #x, __FILE__, __LINE__); \
     } while (0)
+
+// One-time setup per CUDA device, thread-safe. CUDA function attributes (the dynamic
+// shared-memory opt-ins) live in each device's context, so an engine on another device of
+// the same process needs its own; engines may also be driven from several host threads.
+struct PerDeviceOnce {
+    std::atomic<uint64_t> done{0};
+    std::mutex mu;
+    template <typename F>
+    void run(F&& f) {
+        int d = 0;
+        QC_CUDA(cudaGetDevice(&d));
+        const uint64_t bit = uint64_t{1} << (d & 63);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> lk(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        f();
+        done.fetch_or(bit, std::memory_order_release);
+    }
+};
+// SM count of the current device (cached per device).
+inline int device_sm_count() {
+    static std::atomic<int> cache[64];
+    int d = 0;
+    QC_CUDA(cudaGetDevice(&d));
+    int v = cache[d & 63].load(std::memory_order_relaxed);
+    if (!v) {
+        QC_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d));
+        cache[d & 63].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
 
 // Largest simulated subgraph (stored half-state 2^25 amplitudes = 512 MiB fp64).
 constexpr int kMaxQubits = 30;

@@ -822,12 +822,11 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     const bool fp32 = flags & F_FP32;
     if (plan.onchip && fp32) {
         const size_t smem = (size_t{1} << Q) * sizeof(float2);
-        static bool attr32 = false;
-        if (!attr32) {
+        static PerDeviceOnce attr32;
+        attr32.run([] {
             QC_CUDA(cudaFuncSetAttribute(k_onchip_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (1 << 12) * 8));
-            attr32 = true;
-        }
+        });
         if (prof) prof->begin(K_ONCHIP, 0.0, stream);
         k_onchip_f32<<<n_slots, kOnchipThreads, smem, stream>>>(d_slots, d_lp, p, Q, flags | symf, d_out);
         if (prof) prof->end(stream);
@@ -837,14 +836,18 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     if (plan.onchip) {
         const size_t Ns = size_t{1} << Q;
         const size_t smem = Ns * sizeof(double2) + ((flags & F_EXPECT) ? Ns * sizeof(double) : 0);
-        static bool attr_done = false;
-        if (!attr_done) {
+        static PerDeviceOnce attr_done;
+        attr_done.run([] {
             QC_CUDA(cudaFuncSetAttribute(k_onchip, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (1 << 12) * 24));
-            attr_done = true;
-        }
+        });
         const double b = n_slots * N * (((flags & F_INIT) ? 0.0 : 16.0) + ((flags & F_STATE_OUT) ? 16.0 : 0.0));
-        if (prof) prof->begin(K_ONCHIP, b, stream);
+        // no HBM stream: the ceiling is the FP64 pipe (explicit DMUL/DADD) and latency.
+        // Per stored amplitude and layer: phase 6 + RX 6 per target (Q stored bits, + the
+        // mirror op with half-state storage); expectation |a|^2 C(z) 4 + the ordered sum 1
+        const double tq = Q + (plan.sym ? 1.0 : 0.0);
+        const double ops = n_slots * N * (p * (6.0 + 6.0 * tq) + ((flags & F_EXPECT) ? 5.0 : 0.0));
+        if (prof) prof->begin(K_ONCHIP, b, stream, ops);
         k_onchip<<<n_slots, kOnchipThreads, smem, stream>>>(d_slots, d_lp, p, Q, flags | symf,
                                                             d_out);
         if (prof) prof->end(stream);
@@ -853,14 +856,13 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     }
     // (A persistent one-CTA-per-SM variant with a two-stage cp.async ring measured slower
     // on B200: pass A 141 us / pass B 125 us vs 103 / 95 us for these 2-CTA/SM kernels.)
-    static bool attrs = false;
-    if (!attrs) {
+    static PerDeviceOnce attrs;
+    attrs.run([] {
         QC_CUDA(cudaFuncSetAttribute(k_pass_low, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kPassSmem)));
         QC_CUDA(cudaFuncSetAttribute(k_pass_high, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(4096 * sizeof(double2))));
-        attrs = true;
-    }
+    });
     int launches = 0;
     const unsigned grid = static_cast<unsigned>(n_slots) << (Q - 12);
     static const bool v3 = [] {
@@ -878,7 +880,9 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int nmix = cnt(stats ? &stats->mix : nullptr, l);
         // pass A moves a slot if it initialises, phases or mixes it; levels read when phased
         const int active = fa ? n_slots : std::max(nph, nmix);
-        const double ba = (fa ? n_slots * 16.0 : active * 32.0) * N + nph * 2.0 * N;
+        // amplitude bytes: 16 (fp64 complex) or 8 (fp32 mode); f(z) 8 or 4
+        const double ab = fp32 ? 8.0 : 16.0, fb = fp32 ? 4.0 : 8.0;
+        const double ba = (fa ? n_slots * ab : active * 2.0 * ab) * N + nph * 2.0 * N;
         // FP64: 6 per amplitude for the phase, 6 per amplitude per RX target (12 targets)
         const double oa = (nph * 6.0 + nmix * 72.0) * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream, oa);
@@ -896,9 +900,9 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             if (last && (flags & F_STATE_OUT)) fh |= F_STATE_OUT;
             double bh;
             if (fh & F_EXPECT)  // read state, write f (+ state), read levels
-                bh = n_slots * N * (16.0 + 8.0 + 2.0 + ((fh & F_STATE_OUT) ? 16.0 : 0.0));
+                bh = n_slots * N * (ab + fb + 2.0 + ((fh & F_STATE_OUT) ? ab : 0.0));
             else
-                bh = nmix * 32.0 * N;
+                bh = nmix * 2.0 * ab * N;
             int items = 0;
             for (int b = 0; b < kHighBits; ++b) items += plan.high[h].kind[b] != 0 ? 1 : 0;
             // 6 per amplitude per pair op (RX target or mirror), + |a|^2 C(z) (4) when f is emitted
@@ -928,16 +932,14 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         const int nbl = 1 << (Q - 12);
         const int bpw = std::min(32, nbl);
         const int warps = (nbl / bpw) * (plan.sym ? 2 : 1) * n_slots;
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            QC_CUDA(cudaGetDevice(&dev));
-            QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int sms = device_sm_count();
+        static PerDeviceOnce sum_attrs;
+        sum_attrs.run([] {
             QC_CUDA(cudaFuncSetAttribute(k_blocksum<3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sum_smem<3, 8>())));
             QC_CUDA(cudaFuncSetAttribute(k_blocksum<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sum_smem<6, 8>())));
-        }
+        });
         // stages x 1 KB-per-lane chunks: 6 deep when every warp has an SM to itself, else
         // 3 (two warp-CTAs per SM). Smaller stages measured slower at every size
         // (profiles/r1_blocksum_stages.txt).

@@ -1030,15 +1030,12 @@ void set_attrs() {
                                  static_cast<int>(v4::kSmem)));
 }
 int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QC_CUDA(cudaGetDevice(&dev));
-        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    static PerDeviceOnce attrs;
+    attrs.run([] {
         set_attrs<double2>();
         set_attrs<float2>();
-    }
-    return sms;
+    });
+    return device_sm_count();
 }
 // Slots per launch such that every CTA's contiguous tile range spans <= kDescCap slots
 // (a CTA spans at most slots/grid + 3).
@@ -1094,12 +1091,11 @@ bool tma_pass_a(bool fp32, int Q) {
 }
 template <typename V>
 void a5_attr() {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    attr.run([] {
         QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(v4::kSmem + 1024)));
-        attr = true;
-    }
+    });
 }
 }  // namespace
 
@@ -1151,12 +1147,11 @@ using B5Kernel = void (*)(const SlotDesc*, const LayerParam*, int, int, HighPass
                           v4::B5Geo, CUtensorMap);
 template <typename V, int NT, int HM>
 B5Kernel b5_kernel() {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce attr;
+    attr.run([] {
         QC_CUDA(cudaFuncSetAttribute(v4::k_pass_b5<V, NT, HM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(v4::kSmem + 1024)));
-        attr = true;
-    }
+    });
     return v4::k_pass_b5<V, NT, HM>;
 }
 template <typename V>

@@ -315,6 +315,15 @@ int kcap_of(const qc_run_config* c, int max_width) {
     return static_cast<int>(std::min<uint64_t>(classes, static_cast<uint64_t>(c->top_k)));
 }
 
+// widest piece of the chain partition (partition.hpp:58-103), without building it
+int max_width(int n, int M, const qc_run_config* c) {
+    std::vector<int32_t> a, b;
+    chain_intervals(n, M, c->partition_mode, a, b);
+    int w = 1;
+    for (size_t i = 0; i < a.size(); ++i) w = std::max(w, b[i] - a[i] + 1);
+    return w;
+}
+
 // pipeline.hpp:239-263 per-subgraph options for subgraphs [begin, end)
 std::vector<SolveOut> solve_range(qc_engine* e, const Partition& P, const qc_run_config* c,
                                   int begin, int end) {
@@ -524,6 +533,7 @@ struct qc_pipeline {
     qcg::DevBuf tables;  // resident device cut tables of every subgraph
     std::vector<DevGraph> dg;
     double partition_s = 0.0;
+    std::vector<SolveOut> last;  // SolveResults of the last execute (qc_pipeline_records)
 };
 
 extern "C" {
@@ -572,7 +582,8 @@ int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment
         r.partition_s = pl->partition_s;
         r.subgraphs = static_cast<int32_t>(pl->P.first.size());
         auto t0 = std::chrono::steady_clock::now();
-        const auto solves = solve_prepared(e, pl->P.local, pl->dg, pl->opts);
+        pl->last = solve_prepared(e, pl->P.local, pl->dg, pl->opts);
+        const auto& solves = pl->last;
         r.qaoa_s = seconds_since(t0);
         for (const auto& s : solves) r.evals += static_cast<uint64_t>(s.evals);
         t0 = std::chrono::steady_clock::now();
@@ -599,6 +610,38 @@ void qc_pipeline_destroy(qc_pipeline* pl) {
 
 int64_t qc_record_bytes(int top_k_cap, int layers) { return record_bytes(top_k_cap, layers); }
 
+int qc_run_record_bytes(const qc_graph* g, const qc_run_config* cfg, int64_t* bytes,
+                        int32_t* subgraphs) {
+    return guarded([&] {
+        check_config(cfg);
+        if (!bytes) config_error("null argument");
+        const HostGraph hg = load_graph(g);
+        const int M = cfg->subgraphs != 0 ? cfg->subgraphs : derive_subgraph_count(hg.n, cfg->qubit_cap);
+        *bytes = record_bytes(kcap_of(cfg, max_width(hg.n, M, cfg)), cfg->layers);
+        if (subgraphs) *subgraphs = M;
+    });
+}
+
+int qc_pipeline_records(const qc_pipeline* pl, void* records, int64_t capacity, int64_t* bytes,
+                        int32_t* subgraphs) {
+    return guarded([&] {
+        if (!pl) config_error("null pipeline");
+        const int M = static_cast<int>(pl->P.first.size());
+        int maxw = 1;
+        for (const auto& L : pl->P.local) maxw = std::max(maxw, L.n);
+        const int kcap = kcap_of(&pl->cfg, maxw);
+        const int64_t rb = record_bytes(kcap, pl->cfg.layers);
+        if (bytes) *bytes = rb;
+        if (subgraphs) *subgraphs = M;
+        if (!records) return;
+        if (pl->last.size() != static_cast<size_t>(M)) config_error("pipeline has not been executed");
+        if (capacity < rb * M) config_error("record buffer too small");
+        for (int i = 0; i < M; ++i)
+            pack_record(pl->last[static_cast<size_t>(i)], kcap, pl->cfg.layers,
+                        static_cast<char*>(records) + static_cast<int64_t>(i) * rb);
+    });
+}
+
 int qc_shard_range(int M, int shard_index, int shard_count, int32_t* begin, int32_t* end) {
     return guarded([&] {
         if (M < 0 || shard_count < 1 || shard_index < 0 || shard_index >= shard_count)
@@ -611,7 +654,7 @@ int qc_shard_range(int M, int shard_index, int shard_count, int32_t* begin, int3
 }
 
 int qc_shard_solve(qc_engine* e, const qc_graph* g, const qc_run_config* cfg, int32_t begin,
-                   int32_t end, void* records, int32_t* subgraphs) {
+                   int32_t end, void* records, int64_t capacity, int32_t* subgraphs) {
     return guarded([&] {
         if (!e) config_error("null engine");
         QC_CUDA(cudaSetDevice(e->device));
@@ -626,6 +669,9 @@ int qc_shard_solve(qc_engine* e, const qc_graph* g, const qc_run_config* cfg, in
         for (const auto& L : P.local) maxw = std::max(maxw, L.n);
         const int kcap = kcap_of(cfg, maxw);
         const int64_t rb = record_bytes(kcap, cfg->layers);
+        if (capacity < rb * (end - begin))
+            config_error("record buffer holds " + std::to_string(capacity) + " bytes, the shard needs " +
+                         std::to_string(rb * (end - begin)) + " (qc_run_record_bytes)");
         if (begin == end) return;
         const auto solves = solve_range(e, P, cfg, begin, end);
         for (size_t k = 0; k < solves.size(); ++k)
@@ -634,7 +680,8 @@ int qc_shard_solve(qc_engine* e, const qc_graph* g, const qc_run_config* cfg, in
 }
 
 int qc_merge_records(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
-                     const void* records, int32_t M, qc_run_report* report, char* assignment) {
+                     const void* records, int64_t capacity, int32_t M, qc_run_report* report,
+                     char* assignment) {
     return guarded([&] {
         if (!e) config_error("null engine");
         QC_CUDA(cudaSetDevice(e->device));
@@ -645,6 +692,9 @@ int qc_merge_records(qc_engine* e, const qc_graph* g, const qc_run_config* cfg,
         for (const auto& L : P.local) maxw = std::max(maxw, L.n);
         const int kcap = kcap_of(cfg, maxw);
         const int64_t rb = record_bytes(kcap, cfg->layers);
+        if (capacity < rb * M)
+            config_error("record buffer holds " + std::to_string(capacity) + " bytes, " +
+                         std::to_string(M) + " records need " + std::to_string(rb * M));
         std::vector<SolveOut> solves;
         for (int i = 0; i < M; ++i)
             solves.push_back(unpack_record(static_cast<const char*>(records) + static_cast<int64_t>(i) * rb,

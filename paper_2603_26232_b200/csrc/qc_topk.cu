@@ -298,12 +298,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_topk_small_keys(const Key* __
 template <int KT, typename V>
 int launch_small(const V* d_state, int q, bool sym, bool fold, uint64_t classes, int k,
                  Key* keys, cudaStream_t stream) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        QC_CUDA(cudaGetDevice(&dev));
-        QC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
+    const int sms = device_sm_count();
     const uint64_t want = (classes + 8 * kSmallThreads - 1) / (8 * kSmallThreads);  // >= 8 per thread
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(want, 2u * sms)));
     Key* part = keys + 1024;  // stage-1 lists (grid * k keys), final list at keys[0..k)

@@ -46,12 +46,11 @@ def gather_records(local: np.ndarray, bounds, record_bytes: int, rank: int, devi
 def solve_sharded(engine, n: int, edges, rank: int, world: int, device=None, **cfg):
     """One distributed solve: shard the QAOA stage, gather records, merge on rank 0.
     Returns the RunReport on rank 0, None elsewhere."""
-    from . import kcap_for
-    M = engine.subgraph_count(n, edges, **cfg)
+    # record geometry from the same chain partition the C side packs with (widest piece,
+    # not the qubit cap: the two differ whenever the pieces are narrower than the cap)
+    rb, M = engine.run_record_bytes(n, edges, **cfg)
     bounds = shard_bounds(engine, M, world)
     begin, end = bounds[rank]
-    kcap = kcap_for(cfg.get("qubit_cap", 20), cfg.get("top_k", 2), cfg.get("fold", True))
-    rb = engine.record_bytes(kcap, cfg.get("layers", 3))
     rec = engine.shard_solve(n, edges, begin, end, rb, **cfg)
     allrec = gather_records(rec, bounds, rb, rank, device=device)
     if rank == 0:

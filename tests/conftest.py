@@ -19,13 +19,36 @@ def pytest_configure(config):
 
 
 @pytest.fixture(scope="session")
-def oracle():
+def restatement():
+    """oracle/qcut_oracle.c (the C restatement), pinned by the -m "not gpu" tests against
+    the golden vectors the reference produced and against oracle/_ref directly."""
     from oracle.refpy import OracleLib, oracle_available
     if not oracle_available():
         import subprocess
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True,
                        capture_output=True)
     return OracleLib()
+
+
+@pytest.fixture(scope="session")
+def reference_checker(restatement):
+    """The GPU parity checker: the reference build itself (oracle/_ref, which travels to
+    the GPU box in the repo snapshot) whenever it is present, else the restatement."""
+    from oracle.refpy import checker
+    return checker()
+
+
+def _is_gpu_module(module) -> bool:
+    marks = getattr(module, "pytestmark", [])
+    marks = marks if isinstance(marks, list) else [marks]
+    return any(getattr(m, "name", "") == "gpu" for m in marks)
+
+
+@pytest.fixture(scope="module")
+def oracle(request, restatement, reference_checker):
+    """-m gpu modules: the reference build (RefChecker); CPU modules: the restatement
+    under test."""
+    return reference_checker if _is_gpu_module(request.module) else restatement
 
 
 @pytest.fixture(scope="session")

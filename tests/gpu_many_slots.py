@@ -11,12 +11,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle.refpy import OracleLib  # noqa: E402
+from oracle.refpy import checker  # noqa: E402
 from paper_2603_26232_b200 import Engine  # noqa: E402
 
 
 def main():
-    orc = OracleLib()
+    orc = checker()  # the reference build (oracle/_ref) when present
     eng = Engine(0)
     q, p, n = 14, 2, 3200
     e = orc.generate_er(q, 0.3, 5)

@@ -42,7 +42,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_abi_version_and_cap(lib):
-    assert lib.qc_abi_version() == 1
+    assert lib.qc_abi_version() == 2
     assert lib.qc_qubit_cap() >= 26  # BASELINE config 5 needs 26 qubits
 
 

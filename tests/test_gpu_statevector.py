@@ -181,8 +181,11 @@ def test_identity_layers_in_multipass_chains(engine, oracle, q):
 @pytest.mark.parametrize("env", [{"QCG_PASS_B": "tma"},
                                  {"QCG_PASS_B": "tma", "QCG_B5_STORE": "stg"},
                                  {"QCG_PASS_B": "v4"},
-                                 {"QCG_GRAPH": "0", "QCG_PASS_A": "v4"}],
-                         ids=["tma-tensor-store", "tma-register-store", "v4", "direct-launch-v4-pass-a"])
+                                 {"QCG_GRAPH": "0", "QCG_PASS_A": "v4"},
+                                 {"QCG_PASS_B": "tma", "QCG_B5_EARLY": "1"},
+                                 {"QCG_PASS_B": "tma", "QCG_B5_EARLY": "0"}],
+                         ids=["tma-tensor-store", "tma-register-store", "v4", "direct-launch-v4-pass-a",
+                              "tma-early-refill", "tma-no-early-refill"])
 def test_pass_b_kernel_variants(env):
     """Every pass B kernel (qc_pass.cu: TMA boxes with tensor or register stores, v4
     per-thread gathers), and the chain without CUDA-graph capture and with the v4 pass A,
@@ -223,3 +226,32 @@ def test_graph_replay_across_graphs_and_shapes(engine, oracle):
         for k in range(3):
             x0 = oracle.run_ansatz(q, e, prm[k, :2], prm[k, 2:], want_amps=False)[1]
             assert got[k] == x0, (q, k, got[k], x0)
+
+
+# ---- CostTable (statevector.hpp:75-111), direct ---------------------------------------
+@pytest.mark.parametrize("case", ["er20", "weighted_int18", "over_65535", "fractional16"])
+def test_cost_table_matches_reference(engine, oracle, case):
+    """The device cut table (k_levels) against the reference's CostTable on the same graph:
+    the integral uint16 path (q=20 ER; integer weights), the total-weight > 65535 fallback
+    to the double table (statevector.hpp:84-89; test_statevector.cpp:72-80), and
+    fractional weights summed in edge-list order (statevector.hpp:101-110). Bit-exact."""
+    rng = np.random.default_rng(20)
+    if case == "er20":
+        n, e = 20, oracle.generate_er(20, 0.3, 2)
+    elif case == "weighted_int18":
+        n = 18
+        e = [(u, v, float(rng.integers(1, 50))) for u in range(n) for v in range(u + 1, n)
+             if rng.random() < 0.3]
+    elif case == "over_65535":
+        n = 16
+        e = [(u, v, float(rng.integers(900, 1400))) for u in range(n) for v in range(u + 1, n)]
+        assert sum(w for _, _, w in e) > 65535
+    else:
+        n = 16
+        e = [(u, v, 0.1 + rng.random()) for u in range(n) for v in range(u + 1, n)
+             if rng.random() < 0.4]
+    want, wint, wmax = oracle.cost_table(n, e)
+    got, gint, gmax = engine.cost_table(n, e)
+    assert gint == wint == (case in ("er20", "weighted_int18"))
+    assert gmax == wmax
+    assert np.array_equal(got, want)
