@@ -447,6 +447,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="64: exact fp64 (the parity path, default); 32: optional fp32 mode (1e-4)")
+    ap.add_argument("--mixer", default="rx", choices=["rx", "wht"],
+                    help="fp32 mode's mixer form: rx (mixer_pair rotations, default) or wht "
+                         "(Walsh-Hadamard: H diag H with add/sub butterflies; --precision 32)")
     ap.add_argument("--report", default="",
                     help="also write the run as an ExperimentReport JSON v1 (report.hpp) with a "
                          "'gpu' section to this path")
@@ -483,6 +486,8 @@ def main():
     coll_dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
     eng = Engine(local)
     eng.set_precision(args.precision)
+    if args.mixer != "rx":
+        eng.set_mixer(args.mixer)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=local)
     edges = workload_graph(w)
     cfg = dict(qubit_cap=w["qubit_cap"], top_k=w["top_k"], layers=w["layers"],
@@ -612,11 +617,16 @@ def main():
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9 if d["ms"] > 0 else 0.0
     fp_tag = "f64" if args.precision == 64 else "f32"
     traffic, traffic_src = None, None
-    try:  # ncu DRAM bytes per launch of THIS workload's dominant kernel (tools/ncu_traffic.py)
+    try:  # ncu DRAM bytes of THIS workload's dominant kernel (tools/ncu_traffic.py)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(f"{w['key']}/{fp_tag}/{dom}")
-        if tr:
-            traffic, traffic_src = tr.get("dram_bytes_per_launch"), tr.get("source")
+        if tr and tr.get("traffic_over_algorithmic") and d["launches"]:
+            # ncu's DRAM/algorithmic ratio for the same kernel at this workload's launch
+            # shape, times this step's algorithmic bytes per launch
+            traffic = tr["traffic_over_algorithmic"] * d["bytes"] / d["launches"]
+            traffic_src = (f"{tr.get('source')}; DRAM/algorithmic = "
+                           f"{tr['traffic_over_algorithmic']:.3f} x this step's algorithmic "
+                           f"bytes per launch")
     except Exception:
         pass
     fp64_peak = FP64_PEAK_TOPS
@@ -689,7 +699,7 @@ def main():
         "ms_per_step": sec_per_step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64" if args.precision == 64 else "f32",
         "data": "synthetic (graph.hpp:146 ER generator restated in qc_generate_er)",
-        "config": config_dict(w, world), "l2": l2,
+        "config": config_dict(w, world), "l2": l2, "mixer": args.mixer,
         "solve_time_s": sec_per_step, "cut": rep.cut, "evals_per_step": evals_per_step,
         "step_ms": [round(t * 1e3, 2) for t in t_val],
         "host_s_per_step": {k: (v / args.steps if k != "chunk_steps" else v // args.steps)

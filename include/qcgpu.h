@@ -177,6 +177,16 @@ int qc_engine_set_memory_budget(qc_engine* e, uint64_t bytes);
  * mode (float amplitudes, FMA; expectations within 1e-4 relative). The statevector-level
  * calls (qc_run_ansatz, qc_apply_*) always use fp64. Config error for other values. */
 int qc_engine_set_precision(qc_engine* e, int bits);
+/* Mixer form of the fp32 mode (replaces apply_mixer_layer,
+ * statevector.hpp:187-221, behind the fp32 flag): QC_MIXER_RX (0, default) applies
+ * mixer_pair rotations per target; QC_MIXER_WHT (1) applies RX(β)^{(x)T} =
+ * H^{(x)T} diag(2^-n e^{-iβ(n-2|k|)}) H^{(x)T} with add/sub-only butterflies (per register
+ * round in the streaming passes, over the whole state in the on-chip kernel). Config error
+ * for other values, or for WHT while the precision is 64 (not bit-exact); setting
+ * precision 64 resets the mixer to RX. */
+#define QC_MIXER_RX 0
+#define QC_MIXER_WHT 1
+int qc_engine_set_mixer(qc_engine* e, int mixer);
 int qc_engine_profile(qc_engine* e, int on);
 int qc_engine_profile_read(qc_engine* e, int kind, uint64_t* launches, double* ms,
                            double* bytes);
@@ -349,7 +359,9 @@ int qc_gather_topk(qc_comm* c, const void* local, int32_t count, int32_t M, int6
  * all-gather over comms (NCCL; comms[i] = rank i on engines[i], from
  * qc_comm_create_all) -> merge on engines[0]. comms == NULL (engines that share a
  * device, where NCCL cannot form a communicator): the records are concatenated in host
- * memory instead. Same results as qc_run_pipeline. */
+ * memory instead. An engine listed for several shards runs them back to back on one host
+ * thread (an engine is never driven by two threads at once). Same results as
+ * qc_run_pipeline. */
 int qc_run_pipeline_multi(qc_engine* const* engines, qc_comm* const* comms, int n,
                           const qc_graph* g, const qc_run_config* cfg, qc_run_report* report,
                           char* assignment);

@@ -130,6 +130,7 @@ EXPORTED_SYMBOLS = [
     "qc_engine_set_precision", "qc_engine_profile_read_fp64", "qc_run_record_bytes",
     "qc_pipeline_records", "qc_comm_id", "qc_comm_create", "qc_comm_create_all",
     "qc_comm_rank", "qc_comm_destroy", "qc_gather_topk", "qc_run_pipeline_multi",
+    "qc_engine_set_mixer",
 ]
 
 KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
@@ -350,6 +351,12 @@ class Engine:
         """64: exact fp64 (default); 32: optional fp32 mode for solve/eval (1e-4)."""
         self._call("qc_engine_set_precision", C.c_int(bits))
 
+    def set_mixer(self, mixer: str | int):
+        """fp32 mode's mixer form: "rx" (0, mixer_pair rotations) or "wht" (1, the
+        Walsh-Hadamard form H diag H with add/sub butterflies); precision 32 first."""
+        m = {"rx": 0, "wht": 1}.get(mixer, mixer) if isinstance(mixer, str) else int(mixer)
+        self._call("qc_engine_set_mixer", C.c_int(m))
+
     def set_memory_budget(self, nbytes: int):
         self._call("qc_engine_set_memory_budget", C.c_uint64(nbytes))
 
@@ -515,7 +522,7 @@ class Engine:
         structs = (_Graph * n)()
         opts = (_SolveOptions * n)()
         res = (_SolveResult * n)()
-        keep = []
+        keep, bufs = [], []
         for i, ((nv, edges), o) in enumerate(zip(graphs, options)):
             gs, e = _graph(nv, edges)
             structs[i] = gs
@@ -526,13 +533,13 @@ class Engine:
             b = np.zeros(k, np.uint32)
             pr = np.zeros(k)
             pa = np.zeros(2 * max(so.layers, 1))
-            keep += [b, pr, pa]
+            bufs.append((b, pr, pa))
             res[i] = _SolveResult(0, 0, 0, 0, 0.0, b.ctypes.data, pr.ctypes.data, pa.ctypes.data)
         self._call("qc_solve_batch", structs, C.c_int(n), opts, res)
         out = []
         for i in range(n):
             r = res[i]
-            b, pr, pa = keep[n + 3 * i], keep[n + 3 * i + 1], keep[n + 3 * i + 2]
+            b, pr, pa = bufs[i]
             out.append(SolveResult(r.width, bool(r.folded), b[: r.count].copy(),
                                    pr[: r.count].copy(), pa[: 2 * opts[i].layers].copy(),
                                    r.expectation, r.evals))

@@ -87,5 +87,67 @@ __device__ __forceinline__ void rx_local(V (&a)[16], typename Amp<V>::S c, typen
     }
 }
 
+// Walsh–Hadamard mixer variant (fp32 mode only, F_WHT). statevector.hpp's
+// mixer_pair is RX(β) = e^{-iβX} = cos β·I − i sin β·X, and X = H Z H, so on any set T of
+// n register bits RX^{⊗T} = H^{⊗T} · diag_k(2^{-n} e^{-iβ(n − 2|k|)}) · H^{⊗T}, |k| the
+// popcount of k on T, H the unnormalised (+,−) butterfly: two add/sub-only transforms and
+// one complex scale per amplitude instead of n rotations. d[w] = 2^{-n} E^{n−2w} with
+// E = e^{-iβ} = (c, −s).
+__device__ __forceinline__ void wht_diag(float2 (&d)[5], int n, float c, float s) {
+    const float2 E = make_float2(c, -s);
+    const float2 up = make_float2(c * c - s * s, 2.f * c * s);  // E^{-2} = e^{2iβ}
+    float2 x = make_float2(ldexpf(1.f, -n), 0.f);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i < n) x = Amp<float2>::cmul(x, E);
+    d[0] = x;
+#pragma unroll
+    for (int w = 1; w < 5; ++w) d[w] = Amp<float2>::cmul(d[w - 1], up);
+}
+__device__ __forceinline__ void hbfly(float2& x, float2& y) {
+    const float2 t = x;
+    x = make_float2(t.x + y.x, t.y + y.y);
+    y = make_float2(t.x - y.x, t.y - y.y);
+}
+// RX^{⊗T} on the register bits of `opmask` (bits < NB) of a[16]
+template <int NB>
+__device__ __forceinline__ void wht_local(float2 (&a)[16], uint32_t opmask, float c, float s) {
+    float2 d[5];
+    wht_diag(d, __popc(opmask), c, s);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        if (!(opmask & (1u << b))) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) hbfly(a[j], a[j | (1 << b)]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int w = __popc(static_cast<uint32_t>(j) & opmask & ((1u << NB) - 1u));
+        const float2 dj = w == 0 ? d[0] : w == 1 ? d[1] : w == 2 ? d[2] : w == 3 ? d[3] : d[4];
+        a[j] = Amp<float2>::cmul(a[j], dj);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        if (!(opmask & (1u << b))) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            if (!(j & (1 << b))) hbfly(a[j], a[j | (1 << b)]);
+    }
+}
+// the 4-bit register round of the pass kernels: RX butterflies, or (fp32, F_WHT) the
+// Walsh–Hadamard form
+template <typename V>
+__device__ __forceinline__ void mix4(V (&a)[16], typename Amp<V>::S c, typename Amp<V>::S s,
+                                     bool wht) {
+    if constexpr (sizeof(V) == 8) {
+        if (wht) {
+            wht_local<4>(a, 0xFu, c, s);
+            return;
+        }
+    }
+    rx_local<V, 0, 4>(a, c, s);
+}
+
 
 }  // namespace qcg

@@ -223,6 +223,7 @@ int qc_gather_topk(qc_comm* c, const void* local, int32_t count, int32_t M, int6
             config_error("rank " + std::to_string(c->rank) + " holds " + std::to_string(count) +
                          " records, its shard [" + std::to_string(b) + ", " + std::to_string(en) + ") has " +
                          std::to_string(en - b));
+        NvtxRange nv("qcgpu.gather_topk");
         Gather gth{c, M, record_bytes};
         gth.enqueue(local, count);
         gth.collect(all);
@@ -266,9 +267,27 @@ int qc_run_pipeline_multi(qc_engine* const* engines, qc_comm* const* comms, int 
             }
             if (rc[k] != QC_OK) msg[k] = qc_last_error();
         };
+        // one host thread per DISTINCT engine (an engine is driven by one thread at a time):
+        // shards that share an engine object run back to back on that engine's thread
+        std::vector<std::vector<int>> by_engine;
+        for (int i = 0; i < n; ++i) {
+            bool placed = false;
+            for (auto& grp : by_engine)
+                if (engines[grp[0]] == engines[i]) {
+                    grp.push_back(i);
+                    placed = true;
+                    break;
+                }
+            if (!placed) by_engine.push_back({i});
+        }
+        if (comms && by_engine.size() != static_cast<size_t>(n))
+            config_error("an NCCL communicator needs one engine per rank");
+        auto run_group = [&](size_t gi) {
+            for (int i : by_engine[gi]) work(i);
+        };
         std::vector<std::thread> ts;
-        for (int i = 1; i < n; ++i) ts.emplace_back(work, i);
-        work(0);
+        for (size_t gi = 1; gi < by_engine.size(); ++gi) ts.emplace_back(run_group, gi);
+        run_group(0);
         for (auto& t : ts) t.join();
         for (int i = 0; i < n; ++i)
             if (rc[static_cast<size_t>(i)] != QC_OK) throw Error(rc[static_cast<size_t>(i)], msg[static_cast<size_t>(i)]);

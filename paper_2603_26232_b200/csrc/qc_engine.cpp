@@ -573,6 +573,7 @@ void validate_solve(const std::vector<HostGraph>& hg, const std::vector<qc_solve
 std::vector<SolveOut> solve_batch(qc_engine* e, const std::vector<HostGraph>& hg,
                                   const std::vector<qc_solve_options>& opts) {
     validate_solve(hg, opts);
+    NvtxRange r("qcgpu.solve_batch");
     const std::vector<DevGraph> dg = e->prepare(hg, true);
     return solve_prepared(e, hg, dg, opts);
 }
@@ -591,7 +592,10 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
         tol[i] = opts[i].tolerance;
     }
     const auto t0 = std::chrono::steady_clock::now();
-    const auto best = optimize_batch(e, dg, layers, budget, seeds, tol, nullptr, nullptr);
+    const auto best = [&] {
+        NvtxRange nv("qcgpu.optimize (lockstep Nelder-Mead)");
+        return optimize_batch(e, dg, layers, budget, seeds, tol, nullptr, nullptr);
+    }();
     const auto t1 = std::chrono::steady_clock::now();
     e->t_optimize_s += std::chrono::duration<double>(t1 - t0).count();
     struct FinalTimer {
@@ -599,6 +603,7 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
         std::chrono::steady_clock::time_point t;
         ~FinalTimer() { e->t_final_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t).count(); }
     } final_timer{e, t1};
+    NvtxRange nv_final("qcgpu.final_circuits_topk");
 
     // final circuit at the best angles (qaoa.hpp:208) + top-K (qaoa.hpp:211)
     std::vector<SolveOut> out(n);
@@ -756,6 +761,17 @@ int qc_engine_set_precision(qc_engine* e, int bits) {
         check_engine(e);
         if (bits != 64 && bits != 32) config_error("precision must be 64 (exact) or 32 (fp32 mode)");
         e->precision = bits;
+        if (bits == 64) e->mixer = 0;  // the exact path replays mixer_pair only
+    });
+}
+
+int qc_engine_set_mixer(qc_engine* e, int mixer) {
+    return guarded([&] {
+        check_engine(e);
+        if (mixer != 0 && mixer != 1) config_error("mixer must be 0 (RX butterflies) or 1 (Walsh-Hadamard)");
+        if (mixer == 1 && e->precision != 32)
+            config_error("the Walsh-Hadamard mixer is an fp32-mode variant (not bit-exact): set precision 32 first");
+        e->mixer = mixer;
     });
 }
 

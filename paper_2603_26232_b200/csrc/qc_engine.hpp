@@ -152,7 +152,10 @@ struct qc_engine {
     // 64: the exact fp64 path (default, bit-identical to the reference); 32: optional fp32
     // mode for the batched solve/eval paths (statevector-level calls stay fp64)
     int precision = 64;
-    uint32_t fp_flag() const { return precision == 32 ? qcg::F_FP32 : 0u; }
+    int mixer = 0;  // QC_MIXER_RX / QC_MIXER_WHT (fp32 mode only)
+    uint32_t fp_flag() const {
+        return precision == 32 ? (qcg::F_FP32 | (mixer == 1 ? qcg::F_WHT : 0u)) : 0u;
+    }
     void sync();
 };
 

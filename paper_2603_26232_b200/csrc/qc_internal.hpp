@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -12,6 +13,15 @@
 #include <vector>
 
 namespace qcg {
+
+// NVTX ranges around the hot-path stages (SURVEY 5 tracing row): visible under nsys / ncu
+// --nvtx; the header-only NVTX v3 API is a no-op branch when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Status-coded exception; the C-ABI layer maps it to QC_ERR_* (qcgpu.h).
 struct Error : std::runtime_error {
@@ -98,6 +108,7 @@ enum : uint32_t {
     F_TSTORE = 128u,    // pass B (TMA): results leave by tensor stores (default)
     F_B5EARLY = 512u,   // pass B (TMA): refill a stored stage before the next tile's wait
     F_NOLEVREG = 256u,  // pass B (v4) f pass: levels read after the refill (experiment)
+    F_WHT = 1024u,      // fp32 mode only: Walsh–Hadamard form of the RX mixer (qc_amp.cuh)
 };
 
 // One high (gather) pass: 3 column bits (0,1,2) + kHighBits tile bits.

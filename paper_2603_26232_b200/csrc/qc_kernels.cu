@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip_f32(const SlotDesc* _
     const uint32_t N = 1u << Q;
     float2* sa = smemf;
     __shared__ double red[kOnchipThreads / 32];
+    __shared__ float2 dtab[16];  // F_WHT: diagonal by popcount
     const SlotDesc S = slots[blockIdx.x];
     float2* gst = reinterpret_cast<float2*>(S.state);
     const bool sym = flags & F_SYM;
@@ -264,6 +265,40 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip_f32(const SlotDesc* _
         }
         __syncthreads();
         if (!L.mix) continue;
+        if (flags & F_WHT) {
+            // Walsh–Hadamard form over the whole stored state (qc_amp.cuh wht_local): the RX
+            // layer on the Q stored bits and the mirror op (cI - isP, P = the complement = X
+            // on every stored bit, eigenvalue (-1)^|k|) are diagonal after H^{(x)Q}:
+            // d(|k| = w) = 2^-Q E^{Q - 2w + (sym ? (-1)^w : 0)}, E = e^{-iβ} = (c, -s)
+            if (tid <= static_cast<uint32_t>(Q)) {
+                const int w = static_cast<int>(tid);
+                const int m = Q - 2 * w + (sym ? ((w & 1) ? -1 : 1) : 0);
+                double xr = 1.0, xi = 0.0;
+                const double er = L.c, ei = m >= 0 ? -L.s : L.s;
+                for (int i = 0; i < (m >= 0 ? m : -m); ++i) {
+                    const double t = xr * er - xi * ei;
+                    xi = xr * ei + xi * er;
+                    xr = t;
+                }
+                const double sc = ldexp(1.0, -Q);
+                dtab[w] = make_float2(static_cast<float>(xr * sc), static_cast<float>(xi * sc));
+            }
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int t = 0; t < Q; ++t) {
+                    const uint32_t half = 1u << t, lo = half - 1u;
+                    for (uint32_t k = tid; k < N / 2; k += kOnchipThreads) {
+                        const uint32_t i = ((k & ~lo) << 1) | (k & lo);
+                        hbfly(sa[i], sa[i | half]);
+                    }
+                    __syncthreads();
+                }
+                if (pass == 0) {
+                    for (uint32_t k = tid; k < N; k += kOnchipThreads) sa[k] = A::cmul(sa[k], dtab[__popc(k)]);
+                    __syncthreads();
+                }
+            }
+            continue;
+        }
         for (int t = 0; t < Q; ++t) {
             const uint32_t half = 1u << t, lo = half - 1u;
             for (uint32_t k = tid; k < N / 2; k += kOnchipThreads) {
@@ -889,7 +924,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         if (v3)
             k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
         else
-            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & F_FP32), n_slots, stream, pdl_ok && l > 0,
+            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok && l > 0,
                            state_base);
         if (prof) prof->end(stream);
         ++launches;
@@ -912,7 +947,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                 k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
                     d_slots, d_lp, l, Q, plan.high[h], fh);
             else
-                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & F_FP32), n_slots, stream, pdl_ok,
+                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok,
                                state_base);
             if (prof) prof->end(stream);
             ++launches;

@@ -93,6 +93,23 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
+// Phase trace of the pass A tile loop (tools/trace_pass.py; built only with -DQCG_TRACE
+// into a separate tool library): CTAs < kTraceCtas, per group, per local tile, kTraceEv
+// clock64 stamps taken by the group's lane 0.
+#ifdef QCG_TRACE
+constexpr int kTraceCtas = 4, kTraceTiles = 40, kTraceEv = 8;
+__device__ long long g_trace[kTraceCtas * 2 * kTraceTiles * kTraceEv];
+#define QCG_TR(k, ev)                                                                          \
+    do {                                                                                       \
+        if (gt == 0 && blockIdx.x < kTraceCtas && (k) / 2 < kTraceTiles)                       \
+            g_trace[((blockIdx.x * 2 + g) * kTraceTiles + (k) / 2) * kTraceEv + (ev)] = clock64(); \
+    } while (0)
+#else
+#define QCG_TR(k, ev) \
+    do {              \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void grp_sync(uint32_t g) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(g + 1u), "n"(kGT) : "memory");
 }
@@ -151,6 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmask = (1u << tshift) - 1u;
     using S = typename Amp<V>::S;
     const bool init = flags & F_INIT;
+    const bool wht = flags & F_WHT;
     uint32_t t0;
     int cnt;
     tile_range(total_tiles, t0, cnt);
@@ -260,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     a[j] = v;
                 }
             }
-            if (mix) rx_local<V, 0, 4>(a, c, sn);
+            if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[sw<V>(gt * 16u + j)] = a[j];
         }
@@ -271,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
 #pragma unroll
             for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(r | (j << 4))];
-            if (mix) rx_local<V, 0, 4>(a, c, sn);
+            if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[sw<V>(r | (j << 4))] = a[j];
         }
@@ -285,6 +303,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(k + kStages);
         // last target (bit 11 = local bit 3) pair by pair, each pair stored as soon as it
         // is final: spreads the 64 KB of stores over the round instead of one burst
+        if (sizeof(V) == 8 && wht) {
+            if (mix) mix4<V>(a, c, sn, true);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) dst[(j << 8) | gt] = a[j];
+            continue;
+        }
         if (mix) rx_local<V, 0, 3>(a, c, sn);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -330,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
     const bool init = flags & F_INIT;
+    const bool wht = flags & F_WHT;
     uint32_t t0;
     int cnt;
     tile_range(total_tiles, t0, cnt);
@@ -389,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int lut_owner = -1;
     int pending = -1;  // local tile whose refill waits on this group's last bulk store
     for (int k = static_cast<int>(g); k < cnt; k += 2) {
+        QCG_TR(k, 0);
         // refill the stage of this group's previous tile as soon as its bulk store has read
         // it, before waiting for this tile's data
         if (pending >= 0) {
@@ -408,9 +434,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             lut_owner = d.key;
             grp_sync(g);
         }
+        QCG_TR(k, 1);
         while (tag[s] != k) {
         }
         bar_wait(bar0 + s * 8u, static_cast<uint32_t>((k / kStages) & 1));
+        QCG_TR(k, 2);
         if (!act) {
             grp_sync(g);
             issue(k + kStages);
@@ -446,28 +474,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     a[j] = v;
                 }
             }
-            if (mix) rx_local<V, 0, 4>(a, c, sn);
+            if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[ph5<V>(gt * 16u + j)] = a[j];
         }
+        QCG_TR(k, 3);
         __syncwarp();  // round 1 reads only what its own half-warp wrote (e>>8 = gt>>4)
         {
             const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
 #pragma unroll
             for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>(r | (j << 4))];
-            if (mix) rx_local<V, 0, 4>(a, c, sn);
+            if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[ph5<V>(r | (j << 4))] = a[j];
         }
+        QCG_TR(k, 4);
         grp_sync(g);
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>((j << 8) | gt)];
         grp_sync(g);  // the stage's tile is in registers: it becomes the output staging
-        if (mix) rx_local<V, 0, 4>(a, c, sn);
+        QCG_TR(k, 5);
+        if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
         for (int j = 0; j < 16; ++j) st[(j << 8) | gt] = a[j];  // linear, conflict-free
+        QCG_TR(k, 6);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         grp_sync(g);
+        QCG_TR(k, 7);
         if (gt == 0) {
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
                              reinterpret_cast<V*>(d.state) + base),
@@ -517,7 +550,16 @@ __device__ __forceinline__ uint32_t deposit4(uint32_t v, uint32_t mask) {
 // pair ops on local bits of a[16]: local bit b -> gather bit G0 + b (kind != 0 => op)
 template <typename V, int G0, int NB>
 __device__ __forceinline__ void ops_local(V (&a)[16], const HighPass& hp, typename Amp<V>::S c,
-                                          typename Amp<V>::S s) {
+                                          typename Amp<V>::S s, bool wht) {
+    if constexpr (sizeof(V) == 8) {  // fp32 mode, F_WHT: Walsh–Hadamard form over the op bits
+        if (wht) {
+            uint32_t opmask = 0;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) opmask |= (hp.kind[G0 + b] != 0 ? 1u : 0u) << b;
+            wht_local<NB>(a, opmask, c, s);
+            return;
+        }
+    }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         if (hp.kind[G0 + b] == 0) continue;
@@ -546,6 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using S = typename Amp<V>::S;
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
+    const bool wht = flags & F_WHT;
     uint32_t t0;
     int cnt;
     tile_range(total_tiles, t0, cnt);
@@ -700,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // round 0: gather bits 0-3 local
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R0{}, j))];
-        if (mix) ops_local<V, 0, 4>(a, hp, c, sn);
+        if (mix) ops_local<V, 0, 4>(a, hp, c, sn, wht);
         if (nrr == 1) {
             finish(R0{});
             continue;
@@ -711,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // round 1: gather bits 4-7 local
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R1{}, j))];
-        ops_local<V, 4, 4>(a, hp, c, sn);
+        ops_local<V, 4, 4>(a, hp, c, sn, wht);
         if (nrr == 2) {
             finish(R1{});
             continue;
@@ -722,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // round 2: gather bit 8 local (j bit 0); j bits 1-3 carry gather bits 0-2
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = st[sw<V>(e_of(R2{}, j))];
-        ops_local<V, 8, 1>(a, hp, c, sn);
+        ops_local<V, 8, 1>(a, hp, c, sn, wht);
         finish(R2{});
     }
 }
@@ -791,6 +834,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmask = (1u << tshift) - 1u;
     const bool fout = flags & F_EXPECT;
     const bool sout = !fout || (flags & F_STATE_OUT);
+    const bool wht = flags & F_WHT;
     const bool tstore = flags & F_TSTORE;  // results leave by tensor stores of the boxes
     const bool early = flags & F_B5EARLY;  // experiment: refill before the next tile's wait
     uint32_t t0;
@@ -988,7 +1032,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         using R2 = std::integral_constant<int, 2>;
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = at(e_of(R0{}, j));
-        if (mix) ops_local<V, 0, 4>(a, hp, c, sn);
+        if (mix) ops_local<V, 0, 4>(a, hp, c, sn, wht);
         if (nrr == 1) {
             finish(R0{});
             continue;
@@ -998,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         grp_sync(g);
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = at(e_of(R1{}, j));
-        ops_local<V, 4, 4>(a, hp, c, sn);
+        ops_local<V, 4, 4>(a, hp, c, sn, wht);
         if (nrr == 2) {
             finish(R1{});
             continue;
@@ -1008,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         grp_sync(g);
 #pragma unroll
         for (int j = 0; j < 16; ++j) a[j] = at(e_of(R2{}, j));
-        ops_local<V, 8, 1>(a, hp, c, sn);
+        ops_local<V, 8, 1>(a, hp, c, sn, wht);
         finish(R2{});
     }
     if (pending >= 0) {
@@ -1326,4 +1370,14 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     return launches;
 }
 
+#ifdef QCG_TRACE
+extern "C" int qc_trace_read(long long* out, int n) {
+    const int cap = v4::kTraceCtas * 2 * v4::kTraceTiles * v4::kTraceEv;
+    if (n > cap) n = cap;
+    if (cudaMemcpyFromSymbol(out, v4::g_trace, n * sizeof(long long)) != cudaSuccess) return 4;
+    static long long zero[v4::kTraceCtas * 2 * v4::kTraceTiles * v4::kTraceEv] = {};
+    cudaMemcpyToSymbol(v4::g_trace, zero, sizeof(zero));
+    return 0;
+}
+#endif
 }  // namespace qcg

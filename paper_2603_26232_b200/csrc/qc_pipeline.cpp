@@ -85,6 +85,7 @@ void chain_intervals(int n, int M, int mode, std::vector<int32_t>& a, std::vecto
 
 // partition.hpp:111-160 partition
 Partition partition(const HostGraph& g, int M, int mode, int cap) {
+    NvtxRange nv("qcgpu.partition");
     Partition P;
     chain_intervals(g.n, M, mode, P.first, P.last);
     if (cap > 0) {
@@ -349,6 +350,7 @@ std::vector<SolveOut> solve_range(qc_engine* e, const Partition& P, const qc_run
 
 MergeOutput merge_stage(qc_engine* e, const HostGraph& g, const Partition& P,
                         const std::vector<SolveOut>& solves, const qc_run_config* c, bool* windowed) {
+    NvtxRange nv("qcgpu.merge");
     const auto tm0 = std::chrono::steady_clock::now();
     const Pool pool = build_pools(solves);
     std::vector<qc_edge_t> store;

@@ -5,7 +5,7 @@ Checks the engine against the oracle, bit-exact, at subgraph sizes covering ever
 geometry class: mirror passes with 1..8 targets (q = 14..21) and the 9-target pass
 followed by a mirror pass (q = 22); states (F_STATE_OUT) and expectations alone
 (eval_batch: the f pass without the state write); and the fp32 mode's expectations
-(within 1e-4). Prints OK.
+(within 1e-4, RX and Walsh-Hadamard mixers). Prints OK.
 """
 import os
 import sys
@@ -36,15 +36,20 @@ def main():
         got = eng.eval_batch([(q, e)], 2, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
         assert got[0] == x0, f"q={q}: eval_batch {got[0]!r} != {x0!r}"
     # optional fp32 mode (F_FP32): same pass structure on float2 states, within 1e-4
+    # (both mixer forms: RX butterflies and the Walsh-Hadamard variant)
     f32 = Engine(0)
     f32.set_precision(32)
+    wht = Engine(0)
+    wht.set_precision(32)
+    wht.set_mixer("wht")
     for q in (14, 16, 19, 20, 22, 24):
         e = orc.generate_er(q, 0.2, 100 + q)
         rng = np.random.default_rng(q)
         prm = np.concatenate([rng.uniform(0.1, 3.0, 2), rng.uniform(0.1, 3.0, 2)])
         x0 = orc.run_ansatz(q, e, prm[:2], prm[2:], threads=threads, want_amps=False)[1]
-        got = f32.eval_batch([(q, e)], 2, np.zeros(1, np.int32), prm[None, :])
-        assert abs(got[0] - x0) <= 1e-4 * abs(x0), f"fp32 q={q}: {got[0]!r} vs {x0!r}"
+        for name, en in (("rx", f32), ("wht", wht)):
+            got = en.eval_batch([(q, e)], 2, np.zeros(1, np.int32), prm[None, :])
+            assert abs(got[0] - x0) <= 1e-4 * abs(x0), f"fp32 {name} q={q}: {got[0]!r} vs {x0!r}"
     print("OK")
 
 

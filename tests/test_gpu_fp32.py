@@ -55,3 +55,59 @@ def test_precision_rejects_other_widths(engine):
     from paper_2603_26232_b200 import ConfigError
     with pytest.raises(ConfigError):
         engine.set_precision(16)
+
+
+# ---- Walsh-Hadamard mixer variant --------------------------------
+@pytest.fixture
+def eng_wht(engine):
+    engine.set_precision(32)
+    engine.set_mixer("wht")
+    yield engine
+    engine.set_precision(64)  # resets the mixer to RX
+
+
+@pytest.mark.parametrize("q,layers", [(4, 1), (10, 2), (13, 2), (14, 1), (16, 2), (20, 2),
+                                      (21, 1), (22, 2), (24, 1)])
+def test_wht_expectations_within_tolerance(eng_wht, oracle, q, layers):
+    """On-chip whole-state transform (q <= 13), register-round transforms in pass A and
+    pass B (q >= 14; TMA pass A from 22 qubits), against the reference at the same angles."""
+    graphs = [(q, oracle.generate_er(q, 0.3, q + i)) for i in range(2)]
+    rng = np.random.default_rng(100 + q)
+    prm = rng.uniform(0.1, 2.5, size=(4, 2 * layers))
+    idx = np.array([0, 1, 0, 1], np.int32)
+    got = eng_wht.eval_batch(graphs, layers, idx, prm)
+    for k in range(len(idx)):
+        e = graphs[idx[k]][1]
+        _, ref = oracle.run_ansatz(q, e, prm[k, :layers], prm[k, layers:])
+        assert abs(got[k] - ref) <= TOL * abs(ref), (k, got[k], ref)
+
+
+def test_wht_matches_rx_fp32(engine, oracle):
+    """The two fp32 mixer forms agree with each other to fp32 rounding (both 1e-4 of fp64)."""
+    q, layers = 18, 2
+    graphs = [(q, oracle.generate_er(q, 0.4, 7))]
+    prm = np.array([[0.3, 1.1, 0.8, 0.2], [2.0, 0.5, 1.3, 2.9]])
+    idx = np.array([0, 0], np.int32)
+    engine.set_precision(32)
+    try:
+        rx = engine.eval_batch(graphs, layers, idx, prm)
+        engine.set_mixer("wht")
+        wh = engine.eval_batch(graphs, layers, idx, prm)
+    finally:
+        engine.set_precision(64)
+    assert np.allclose(wh, rx, rtol=2e-5, atol=0)
+
+
+def test_wht_pipeline_config1(eng_wht, oracle):
+    edges = oracle.generate_er(100, 0.1, 0)
+    r = eng_wht.run_pipeline(100, edges, qubit_cap=10, top_k=4, layers=1, budget=200, seed=0)
+    assert abs(r.cut - 296.0) <= 0.03 * 296.0
+
+
+def test_wht_requires_fp32(engine):
+    from paper_2603_26232_b200 import ConfigError
+    engine.set_precision(64)
+    with pytest.raises(ConfigError):
+        engine.set_mixer("wht")
+    with pytest.raises(ConfigError):
+        engine.set_mixer(2)
