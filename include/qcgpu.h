@@ -200,6 +200,10 @@ int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t*
 /* Host wall seconds accumulated since the last host_stats reset: [0] lockstep optimise,
  * [1] final circuits + top-K, [2] merge, [3] whole qc_pipeline_execute. */
 int qc_engine_phase_times(const qc_engine* e, double* out4);
+/* Split of qc_engine_host_stats' prep time (same reset): [0] result reads + NM tell,
+ * [1] staging build (cos/sin beta, phase LUTs), [2] launch (staging copy + chain or
+ * CUDA-graph launch, completion event). */
+int qc_engine_host_split(const qc_engine* e, double* out3);
 /* Host<->device bytes copied by this engine since creation. */
 int qc_engine_transfers(const qc_engine* e, uint64_t* h2d, uint64_t* d2h);
 /* The engine's cudaStream_t (all engine work is ordered on it). */

@@ -130,7 +130,7 @@ EXPORTED_SYMBOLS = [
     "qc_engine_set_precision", "qc_engine_profile_read_fp64", "qc_run_record_bytes",
     "qc_pipeline_records", "qc_comm_id", "qc_comm_create", "qc_comm_create_all",
     "qc_comm_rank", "qc_comm_destroy", "qc_gather_topk", "qc_run_pipeline_multi",
-    "qc_engine_set_mixer",
+    "qc_engine_set_mixer", "qc_engine_host_split",
 ]
 
 KERNEL_KINDS = ["levels", "onchip", "pass_low", "pass_high", "blocksum", "finalsum", "topk",
@@ -383,10 +383,13 @@ class Engine:
         w, p_, n = C.c_double(0), C.c_double(0), C.c_uint64(0)
         ph = (C.c_double * 4)()
         _check(self.lib, self.lib.qc_engine_phase_times(self._h, ph))
+        sp = (C.c_double * 3)()
+        _check(self.lib, self.lib.qc_engine_host_split(self._h, sp))
         _check(self.lib, self.lib.qc_engine_host_stats(self._h, C.byref(w), C.byref(p_), C.byref(n),
                                                        C.c_int(int(reset))))
         return dict(wait_s=w.value, prep_s=p_.value, chunk_steps=int(n.value),
-                    optimize_s=ph[0], final_s=ph[1], merge_s=ph[2], execute_s=ph[3])
+                    optimize_s=ph[0], final_s=ph[1], merge_s=ph[2], execute_s=ph[3],
+                    tell_s=sp[0], stage_s=sp[1], launch_s=sp[2])
 
     def transfers(self):
         h = C.c_uint64(0)

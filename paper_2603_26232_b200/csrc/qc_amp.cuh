@@ -8,6 +8,56 @@
 
 namespace qcg {
 
+// Kernel span trace (tool-only -DQCG_TRACE build, tools/trace_spans.py): every CTA group /
+// warp leader appends {kind, block, sm | group << 16, entry ns, exit ns} (globaltimer). One
+// buffer per translation unit (no -rdc), read by qc_span_read_<tu>.
+#ifdef QCG_TRACE
+struct SpanRec {
+    uint32_t kind, block, smg, pad;
+    unsigned long long t0, t1;
+};
+constexpr uint32_t kSpanCap = 1u << 20;
+static __device__ SpanRec g_span[kSpanCap];
+static __device__ unsigned int g_span_n;
+__device__ __forceinline__ unsigned long long span_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void span_end(uint32_t kind, uint32_t grp, unsigned long long t0) {
+    const unsigned i = atomicAdd(&g_span_n, 1u);
+    if (i < kSpanCap) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_span[i] = SpanRec{kind, blockIdx.x, smid | (grp << 16), 0u, t0, span_now()};
+    }
+}
+#define QCG_SPAN_BEGIN() const unsigned long long qcg_span_t0_ = ::qcg::span_now()
+#define QCG_SPAN_END(kind, grp, who)                                   \
+    do {                                                               \
+        if (who) ::qcg::span_end((kind), (grp), qcg_span_t0_);         \
+    } while (0)
+#define QCG_SPAN_READER(name)                                                                 \
+    extern "C" int name(void* out, int cap, int* n) {                                         \
+        unsigned cnt = 0;                                                                     \
+        if (cudaMemcpyFromSymbol(&cnt, ::qcg::g_span_n, sizeof(cnt)) != cudaSuccess) return 4; \
+        cnt = cnt < ::qcg::kSpanCap ? cnt : ::qcg::kSpanCap;                                  \
+        const unsigned m = cnt < static_cast<unsigned>(cap) ? cnt : static_cast<unsigned>(cap); \
+        if (m && cudaMemcpyFromSymbol(out, ::qcg::g_span, m * sizeof(::qcg::SpanRec)) != cudaSuccess) return 4; \
+        *n = static_cast<int>(m);                                                             \
+        const unsigned z = 0;                                                                 \
+        cudaMemcpyToSymbol(::qcg::g_span_n, &z, sizeof(z));                                   \
+        return 0;                                                                             \
+    }
+#else
+#define QCG_SPAN_BEGIN() \
+    do {                 \
+    } while (0)
+#define QCG_SPAN_END(kind, grp, who) \
+    do {                             \
+    } while (0)
+#endif
+
 __device__ __forceinline__ void cpa16(uint32_t s, const void* g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(g) : "memory");
 }

@@ -241,6 +241,7 @@ void qc_engine::reserve(int Q, bool need_fbuf, size_t slots) {
 
 void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
                               uint32_t flags, size_t slot0, ChunkCtx& ctx) {
+    const auto t_enq = std::chrono::steady_clock::now();
     ctx.n = n;
     ctx.flags = flags;
     if (n <= 0) return;
@@ -276,7 +277,9 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     const size_t bytes = o_lut + lut_total * lut_entry;
     // a replayed graph copies a fixed-size staging block: sized for every slot phasing
     // every layer with the longest LUT of the solve, so it does not change step to step
-    const bool graph = use_graphs() && !prof.on;
+    // the ping-pong wait binds to the other chunk's latest pass event at enqueue time, which
+    // a replayed graph cannot express: those chunk steps launch directly
+    const bool graph = use_graphs() && !prof.on && !ctx.passes;
     size_t copy_bytes = bytes;
     if (graph) {
         size_t maxl = 0;
@@ -341,13 +344,15 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             }
         }
     }
+    const auto t_staged = std::chrono::steady_clock::now();
     double* ho = (flags & F_EXPECT) ? static_cast<double*>(ctx.hout.get(static_cast<size_t>(n) * 8)) : nullptr;
+    if (ctx.wait_on) QC_CUDA(cudaStreamWaitEvent(cs, ctx.wait_on, 0));
     auto record = [&](size_t nbytes) {
         h2d_copy(d, h, nbytes, cs);
         const int k = launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
                                    reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
                                    reinterpret_cast<double*>(fb), part, tick, od, cs, &stats,
-                                   graph ? nullptr : &prof, st);
+                                   graph ? nullptr : &prof, st, ctx.passes);
         if (ho) d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
         return k;
     };
@@ -397,6 +402,9 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     }
     if (!ctx.done) QC_CUDA(cudaEventCreateWithFlags(&ctx.done, cudaEventDisableTiming));
     QC_CUDA(cudaEventRecord(ctx.done, cs));
+    const auto t_launched = std::chrono::steady_clock::now();
+    host_stage_s += std::chrono::duration<double>(t_staged - t_enq).count();
+    host_launch_s += std::chrono::duration<double>(t_launched - t_staged).count();
 }
 
 void qc_engine::wait_chunk(ChunkCtx& ctx, double* out) {
@@ -485,6 +493,26 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
             QC_CUDA(cudaEventDestroy(ready));
             for (size_t c = 0; c < nchunks; ++c)
                 ctx(c).st = (c % nstreams) ? e->aux[c % nstreams - 1] : e->stream;
+            // Ping-pong (QCG_PINGPONG=1): whole-GPU pass kernels of concurrently queued chunks
+            // otherwise interleave launch by launch, so the chunks stay in phase, their block
+            // sums finish together and the device idles through every chunk's host step.
+            // Chained on pass events, chunk c's passes follow chunk c-1's, and one chunk's
+            // block sum + host step overlap the next chunk's passes.
+            static const bool pingpong = [] {
+                const char* v = std::getenv("QCG_PINGPONG");
+                return v && v[0] == '1';
+            }();
+            for (size_t c = 0; c < nchunks; ++c) {
+                ChunkCtx& x = ctx(c);
+                if (pingpong && nchunks > 1) {
+                    if (!x.passes) QC_CUDA(cudaEventCreateWithFlags(&x.passes, cudaEventDisableTiming));
+                } else if (x.passes) {
+                    QC_CUDA(cudaEventDestroy(x.passes));
+                    x.passes = nullptr;
+                }
+            }
+            for (size_t c = 0; c < nchunks; ++c)
+                ctx(c).wait_on = (pingpong && nchunks > 1) ? ctx((c + nchunks - 1) % nchunks).passes : nullptr;
             std::vector<std::vector<EvalPoint>> pts(nchunks);
             std::vector<std::vector<size_t>> who(nchunks);
             std::vector<char> inflight(nchunks, 0);
@@ -504,11 +532,21 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                     e->enqueue_chunk(dg, pts[c].data(), static_cast<int>(pts[c].size()), p,
                                      F_INIT | F_EXPECT | e->fp_flag(), c * per, ctx(c));
             };
-            for (size_t c = 0; c < nchunks; ++c) launch(c);
+            // Staggered start (QCG_STAGGER=1): chunk c+1's first step is enqueued only when
+            // chunk c's first step completes. Measured: the interleaving of whole-GPU pass
+            // kernels pulls the chunks back into phase within a few steps (C2 71.3 vs
+            // 71.2 ms), so it is off; the ping-pong below keeps them apart.
+            static const bool stagger = [] {
+                const char* v = std::getenv("QCG_STAGGER");
+                return v && v[0] == '1';
+            }();
+            size_t started = stagger ? 1 : nchunks;
+            for (size_t c = 0; c < started; ++c) launch(c);
             // completion-order service: whichever chunk's step finished is told/asked and
             // re-enqueued first, so the device never idles behind a fixed host order
             size_t live = 0;
             for (size_t c = 0; c < nchunks; ++c) live += inflight[c] ? 1 : 0;
+            live += nchunks - started;  // not yet started (staggered)
             using clk = std::chrono::steady_clock;
             while (live) {
                 size_t c = nchunks;
@@ -521,6 +559,11 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                         else if (q != cudaErrorNotReady) QC_CUDA(q);
                     }
                     if (c != nchunks) break;
+                }
+                if (started < nchunks) {  // staggered start: queue the next chunk first
+                    launch(started);
+                    if (!inflight[started]) --live;
+                    ++started;
                 }
                 const auto tp = clk::now();
                 e->host_wait_s += std::chrono::duration<double>(tp - tw).count();
@@ -536,6 +579,7 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                     }
                     opt[i].tell(f);
                 }
+                e->host_tell_s += std::chrono::duration<double>(clk::now() - tp).count();
                 launch(c);
                 e->host_prep_s += std::chrono::duration<double>(clk::now() - tp).count();
                 ++e->host_steps;
@@ -814,9 +858,19 @@ int qc_engine_host_stats(qc_engine* e, double* wait_s, double* prep_s, uint64_t*
         if (steps) *steps = e->host_steps;
         if (reset) {
             e->host_wait_s = e->host_prep_s = 0.0;
+            e->host_tell_s = e->host_stage_s = e->host_launch_s = 0.0;
             e->host_steps = 0;
             e->t_optimize_s = e->t_final_s = e->t_merge_s = e->t_execute_s = 0.0;
         }
+    });
+}
+
+int qc_engine_host_split(const qc_engine* e, double* out3) {
+    return guarded([&] {
+        if (!e || !out3) config_error("null argument");
+        out3[0] = e->host_tell_s;
+        out3[1] = e->host_stage_s;
+        out3[2] = e->host_launch_s;
     });
 }
 

@@ -84,6 +84,11 @@ struct ChunkCtx {
     uint32_t flags = 0;
     double* d_out = nullptr;
     cudaStream_t st = nullptr;  // stream the chunk runs on (null: the engine stream)
+    // lockstep ping-pong: `passes` is recorded after this chunk's last pass kernel (before
+    // its block sum); the chunk's next step first waits on `wait_on` (the previous chunk's
+    // `passes`), so chunks' pass chains alternate instead of interleaving launch by launch
+    cudaEvent_t passes = nullptr;
+    cudaEvent_t wait_on = nullptr;
     // CUDA graph of this chunk's step (staging upload -> launch chain -> result read),
     // captured once per ChainKey and replayed each lockstep step
     cudaGraphExec_t gexec = nullptr;
@@ -95,6 +100,7 @@ struct ChunkCtx {
     ~ChunkCtx() {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (done) cudaEventDestroy(done);
+        if (passes) cudaEventDestroy(passes);
     }
 };
 
@@ -123,6 +129,9 @@ struct qc_engine {
         return on;
     }
     double host_wait_s = 0.0, host_prep_s = 0.0;  // lockstep loop: waiting vs preparing
+    // split of host_prep_s (QCG_HOST_PROFILE): results read + NM tell, staging build
+    // (cos/sin, phase LUTs), launch (H2D record / graph launch)
+    double host_tell_s = 0.0, host_stage_s = 0.0, host_launch_s = 0.0;
     uint64_t host_steps = 0;
     double t_optimize_s = 0.0, t_final_s = 0.0, t_merge_s = 0.0, t_execute_s = 0.0;
 

@@ -219,7 +219,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                  int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
                  unsigned* d_tickets, double* d_out, cudaStream_t stream,
                  const ChainStats* stats = nullptr, Prof* prof = nullptr,
-                 const void* state_base = nullptr);
+                 const void* state_base = nullptr, cudaEvent_t passes_done = nullptr);
 size_t partials_per_slot(const ChainPlan& plan);
 // v4 streaming passes (qc_pass.cu): persistent, one CTA per SM. pdl: launched with
 // programmatic stream serialization (the kernel's prologue overlaps the previous kernel's

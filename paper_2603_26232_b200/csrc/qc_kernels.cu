@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const SlotDesc* __res
                                                          const LayerParam* __restrict__ lp,
                                                          int p, int Q, uint32_t flags,
                                                          double* __restrict__ out) {
+    QCG_SPAN_BEGIN();
     extern __shared__ double2 smem[];
     const uint32_t N = 1u << Q;
     double2* sa = smem;
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip(const SlotDesc* __res
     }
     if (flags & F_STATE_OUT)
         for (uint32_t e = tid; e < N; e += kOnchipThreads) S.state[e] = sa[e];
+    QCG_SPAN_END(6, 0, threadIdx.x == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -630,6 +632,7 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
                                                 double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
+    QCG_SPAN_BEGIN();
     constexpr int kSumChunk = 16 * kSumParts;  // doubles per chunk per chain
     constexpr size_t kSumStageBytes = sum_stage_bytes<kSumParts>();
     extern __shared__ unsigned char sraw[];
@@ -747,6 +750,7 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
             tickets[slot] = 0u;
         }
     }
+    QCG_SPAN_END(5, 0, lane == 0);
 }
 
 // Encode the f-buffer tensor map (driver entry point resolved once through the runtime).
@@ -846,7 +850,7 @@ size_t partials_per_slot(const ChainPlan& plan) {
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,
                  int n_slots, int p, uint32_t flags, double* d_fbuf, double* d_partials,
                  unsigned* d_tickets, double* d_out, cudaStream_t stream, const ChainStats* stats,
-                 Prof* prof, const void* state_base) {
+                 Prof* prof, const void* state_base, cudaEvent_t passes_done) {
     if (n_slots <= 0) return 0;
     const int Q = plan.Q;
     const double N = static_cast<double>(size_t{1} << Q);
@@ -866,6 +870,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         k_onchip_f32<<<n_slots, kOnchipThreads, smem, stream>>>(d_slots, d_lp, p, Q, flags | symf, d_out);
         if (prof) prof->end(stream);
         QC_CUDA(cudaGetLastError());
+        if (passes_done) QC_CUDA(cudaEventRecord(passes_done, stream));
         return 1;
     }
     if (plan.onchip) {
@@ -887,6 +892,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                                                             d_out);
         if (prof) prof->end(stream);
         QC_CUDA(cudaGetLastError());
+        if (passes_done) QC_CUDA(cudaEventRecord(passes_done, stream));
         return 1;
     }
     // (A persistent one-CTA-per-SM variant with a two-stage cp.async ring measured slower
@@ -954,6 +960,9 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         }
     }
     QC_CUDA(cudaGetLastError());
+    // every pass of the chain is queued: a chunk queued behind this one may start its
+    // passes now (lockstep ping-pong, qc_engine.cpp optimize_batch)
+    if (passes_done) QC_CUDA(cudaEventRecord(passes_done, stream));
     if ((flags & F_EXPECT) && fp32) {
         const int nbl = 1 << (Q - 12);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 4.0, stream);
@@ -994,3 +1003,6 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
 }
 
 }  // namespace qcg
+#ifdef QCG_TRACE
+QCG_SPAN_READER(qc_span_read_kernels)
+#endif

@@ -94,6 +94,12 @@ struct SearchArgs {
     int32_t leaves_per_thread;
     const double* base_acc;   // device acc of fixed prefix (exact path)
     const int64_t* base_iacc; // device acc (integral path)
+    // windows longer than kMaxL levels (level mode with forced chains, e.g. top-K 1: few
+    // leaves, hundreds of levels): per-thread odometer state in global scratch, L entries
+    // per array per thread, instead of local arrays
+    int32_t* sc_i;            // r, c, sel: 3 * L ints per thread
+    int64_t* sc_ips;          // L per thread
+    double* sc_dps;           // L per thread
     uint64_t* blk_idx;        // per-block best leaf index
     double* blk_val;          // per-block best value (exact path / integral as double)
     int64_t* blk_ival;
@@ -136,7 +142,7 @@ __device__ __forceinline__ int vertex_bit(const SearchArgs& A, const int* c, int
     return entry_bit(A, L, c[lvl - A.s], static_cast<int>(x) - L.first);
 }
 
-template <bool INTEGRAL>
+template <bool INTEGRAL, bool LONG>
 __global__ void __launch_bounds__(kSearchThreads) k_search(SearchArgs A, uint64_t total_bound) {
     const int L = A.L;
     const int need0 = need_parity(A);
@@ -159,9 +165,19 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(SearchArgs A, uint64_
     uint64_t bidx = 0;
 
     if (idx0 < T) {
-        int r[kMaxL], c[kMaxL], sel[kMaxL];
-        int64_t ips[kMaxL] = {};  // score_level fills them in level order
-        double dps[kMaxL] = {};
+        int r_l[LONG ? 1 : kMaxL], c_l[LONG ? 1 : kMaxL], sel_l[LONG ? 1 : kMaxL];
+        int64_t ips_l[LONG ? 1 : kMaxL] = {};  // score_level fills them in level order
+        double dps_l[LONG ? 1 : kMaxL] = {};
+        int *r = r_l, *c = c_l, *sel = sel_l;
+        int64_t* ips = ips_l;
+        double* dps = dps_l;
+        if constexpr (LONG) {
+            r = A.sc_i + t * 3 * static_cast<uint64_t>(L);
+            c = r + L;
+            sel = c + L;
+            ips = A.sc_ips + t * static_cast<uint64_t>(L);
+            dps = A.sc_dps + t * static_cast<uint64_t>(L);
+        }
         // decode idx0
         uint64_t rem = idx0;
         int need = need0;
@@ -413,7 +429,7 @@ __global__ void k_cut_int(const uint32_t* __restrict__ eu, const uint32_t* __res
 // Device-side edge classification for the integral windowed/level merge (replaces host
 // bucketing of every edge: merge.hpp:103-113 level_edge_buckets, grouped for the unary /
 // pair tables). Bins: fixed edges of level hi (lo in an earlier window) -> bin hi;
-// in-window edges (hi, lo) -> bin M + hi*kMaxL + (lo - win_start[hi]). Sums over a bin are
+// in-window edges (hi, lo) -> bin M + hi*span + (lo - win_start[hi]). Sums over a bin are
 // integers, so the scatter order is immaterial.
 // ---------------------------------------------------------------------------
 struct ClassArgs {
@@ -425,6 +441,7 @@ struct ClassArgs {
     const int32_t* ws;        // window start of each level
     const int32_t* first;     // first global vertex of each level
     int M;
+    int span;                 // bin stride: the longest window (levels)
 };
 
 __device__ __forceinline__ void classify(const ClassArgs& A, long long k, int& bin, int32_t& khi,
@@ -446,7 +463,7 @@ __device__ __forceinline__ void classify(const ClassArgs& A, long long k, int& b
         bin = lb;
         kx = static_cast<int32_t>(a);  // global id of the fixed endpoint
     } else {
-        bin = A.M + lb * kMaxL + (la - A.ws[lb]);
+        bin = A.M + lb * A.span + (la - A.ws[lb]);
         kx = static_cast<int32_t>(a) - A.first[la];
     }
 }
@@ -610,8 +627,11 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     const size_t total_entries = static_cast<size_t>(bits_off[S(M - 1)] + in.counts[M - 1]);
     std::vector<uint32_t> hbits(in.bits, in.bits + total_entries);
     std::vector<int32_t> win_start(S(M));
-    for (const Window& W : windows)
+    int span = 1;  // longest window (levels)
+    for (const Window& W : windows) {
         for (int i = W.s; i < W.e; ++i) win_start[S(i)] = W.s;
+        span = std::max(span, W.e - W.s);
+    }
 
     // ---- lex-sorted candidate lists per level: parity 0, parity 1, all
     std::vector<int32_t> lists;
@@ -707,10 +727,10 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         auto* d_fl = dupload(keep, fl, st);
         auto* d_ws = dupload(keep, win_start, st);
         auto* d_firstl = dupload(keep, first_l, st);
-        const size_t nbins = S(M) + S(M) * kMaxL;
+        const size_t nbins = S(M) + S(M) * S(span);
         auto* d_hist = dalloc<unsigned>(keep, nbins);
         QC_CUDA(cudaMemsetAsync(d_hist, 0, nbins * 4, st));
-        ClassArgs CA{d_eu, d_ev, d_ew, in.m, d_fl, d_ws, d_firstl, M};
+        ClassArgs CA{d_eu, d_ev, d_ew, in.m, d_fl, d_ws, d_firstl, M, span};
         const unsigned cblocks = static_cast<unsigned>(std::max<long long>(1, std::min<long long>((in.m + 255) / 256, 148 * 16)));
         if (m) {
             prof->begin(K_MERGE_OTHER, static_cast<double>(m) * 16.0, st);
@@ -722,7 +742,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         QC_CUDA(cudaMemcpyAsync(hist.data(), d_hist, nbins * 4, cudaMemcpyDeviceToHost, st));
         QC_CUDA(cudaStreamSynchronize(st));
         *d2h += nbins * 4;
-        // fixed edges: bins [0, M) in level order; pair edges: bins M + hi*kMaxL + (lo-ws)
+        // fixed edges: bins [0, M) in level order; pair edges: bins M + hi*span + (lo-ws)
         std::vector<unsigned> cursor(nbins);
         unsigned nfixed = 0, npair = 0;
         for (int i = 0; i < M; ++i) {
@@ -739,7 +759,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
             WinLevel& L = wl[S(i)];
             L.pair_base = static_cast<int32_t>(pair_off.size());
             for (int j = s0; j <= i; ++j) {
-                const size_t bin = S(M) + S(i) * kMaxL + S(j - s0);
+                const size_t bin = S(M) + S(i) * S(span) + S(j - s0);
                 const unsigned len = hist[bin];
                 cursor[bin] = npair;
                 PairGroup G{i, j, 0, static_cast<int32_t>(npair), static_cast<int32_t>(len)};
@@ -835,9 +855,6 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
     std::vector<Geo> geo;
     unsigned max_blocks = 1;
     for (const Window& W : windows) {
-        if (W.e - W.s > kMaxL)
-            resource_error("merge window spans " + std::to_string(W.e - W.s) + " levels (max " +
-                           std::to_string(kMaxL) + ")");
         const WinLevel& L0 = wl[S(W.s)];
         auto total_for = [&](int sel) {
             uint64_t T = 0;
@@ -851,7 +868,8 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         uint64_t bound = W.need == 2 ? total_for(2)
                          : W.need == 3 ? total_for(0)
                                        : std::max(total_for(0), total_for(1));
-        const uint64_t target_threads = 148ull * 1024;
+        // long windows keep their odometer state in global scratch: fewer threads
+        const uint64_t target_threads = (W.e - W.s > kMaxL) ? 148ull * 64 : 148ull * 1024;
         uint64_t per = (bound + target_threads - 1) / target_threads;
         if (per < 1) per = 1;
         if (per > (1u << 20)) per = 1u << 20;
@@ -891,17 +909,32 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
         A.blk_idx = d_bidx;
         A.blk_val = d_bval;
         A.blk_ival = d_bival;
+        const bool lng = A.L > kMaxL;
+        if (lng) {  // per-thread odometer state for the long window (merge.hpp allows any M)
+            const uint64_t thr = static_cast<uint64_t>(geo[w].blocks) * kSearchThreads;
+            const uint64_t per = thr * static_cast<uint64_t>(A.L);
+            A.sc_i = dalloc<int32_t>(keep, S(per * 3));
+            A.sc_ips = dalloc<int64_t>(keep, S(per));
+            A.sc_dps = dalloc<double>(keep, S(per));
+        }
+        auto search = [&](auto kern) {
+            prof->begin(K_MERGE_SEARCH, static_cast<double>(geo[w].bound) * 8.0, st);
+            kern<<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
+            prof->end(st);
+        };
         if (integral) {
             prof->begin(K_MERGE_OTHER, 0.0, st);
             k_unary<<<static_cast<unsigned>(A.L), 128, 0, st>>>(A, d_intra, d_fixed_edges, d_utab);
             prof->end(st);
-            prof->begin(K_MERGE_SEARCH, static_cast<double>(geo[w].bound) * 8.0, st);
-            k_search<true><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
-            prof->end(st);
+            if (lng)
+                search(k_search<true, true>);
+            else
+                search(k_search<true, false>);
         } else {
-            prof->begin(K_MERGE_SEARCH, static_cast<double>(geo[w].bound) * 8.0, st);
-            k_search<false><<<geo[w].blocks, kSearchThreads, 0, st>>>(A, geo[w].bound);
-            prof->end(st);
+            if (lng)
+                search(k_search<false, true>);
+            else
+                search(k_search<false, false>);
         }
         prof->begin(K_MERGE_OTHER, 0.0, st);
         k_commit<<<1, 1, 0, st>>>(A, static_cast<int>(geo[w].blocks), d_leaves, d_dead, d_acc, d_iacc);

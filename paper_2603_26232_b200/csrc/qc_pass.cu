@@ -99,6 +99,18 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 #ifdef QCG_TRACE
 constexpr int kTraceCtas = 4, kTraceTiles = 40, kTraceEv = 8;
 __device__ long long g_trace[kTraceCtas * 2 * kTraceTiles * kTraceEv];
+// every CTA (globaltimer ns): entry, after the prologue, group 0 done, group 1 done
+constexpr int kTraceMaxCtas = 1024;
+__device__ unsigned long long g_cta[kTraceMaxCtas * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define QCG_CTA(ev, cond)                                                  \
+    do {                                                                   \
+        if ((cond) && blockIdx.x < kTraceMaxCtas) g_cta[blockIdx.x * 4 + (ev)] = gtimer(); \
+    } while (0)
 #define QCG_TR(k, ev)                                                                          \
     do {                                                                                       \
         if (gt == 0 && blockIdx.x < kTraceCtas && (k) / 2 < kTraceTiles)                       \
@@ -107,6 +119,9 @@ __device__ long long g_trace[kTraceCtas * 2 * kTraceTiles * kTraceEv];
 #else
 #define QCG_TR(k, ev) \
     do {              \
+    } while (0)
+#define QCG_CTA(ev, cond) \
+    do {                  \
     } while (0)
 #endif
 
@@ -162,6 +177,7 @@ template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_a(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
              int Q, uint32_t flags, uint32_t total_tiles) {
+    QCG_SPAN_BEGIN();
     extern __shared__ __align__(1024) unsigned char sm[];
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[((j + 8) << 8) | gt] = a[j + 8];
         }
     }
+    QCG_SPAN_END(2, g, gt == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -345,6 +362,7 @@ template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_a5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
               int Q, uint32_t flags, uint32_t total_tiles, const __grid_constant__ CUtensorMap tmap) {
+    QCG_SPAN_BEGIN();
     using A = Amp<V>;
     using S = typename A::S;
     constexpr uint32_t kTileBytes = 4096u * sizeof(V);
@@ -353,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
+    QCG_CTA(0, tid == 0);
     const bool init = flags & F_INIT;
     const bool wht = flags & F_WHT;
     uint32_t t0;
@@ -410,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(1);
     }
 
+    QCG_CTA(1, tid == 0);
     V* slut = reinterpret_cast<V*>(sm + kOffLut) + g * kLutCap;
     int lut_owner = -1;
     int pending = -1;  // local tile whose refill waits on this group's last bulk store
@@ -517,6 +537,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(pending);
     }
     if (gt == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    QCG_CTA(2 + g, gt == 0);
+    QCG_SPAN_END(1, g, gt == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -581,6 +603,7 @@ template <typename V>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_b(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
              int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles) {
+    QCG_SPAN_BEGIN();
     extern __shared__ __align__(1024) unsigned char sm[];
     const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
     const int tshift = Q - 12;
@@ -768,6 +791,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ops_local<V, 8, 1>(a, hp, c, sn, wht);
         finish(R2{});
     }
+    QCG_SPAN_END(3, g, gt == 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -824,6 +848,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     k_pass_b5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
               int Q, const __grid_constant__ HighPass hp, uint32_t flags, uint32_t total_tiles,
               const __grid_constant__ B5Geo geo, const __grid_constant__ CUtensorMap tmap) {
+    QCG_SPAN_BEGIN();
     using A = Amp<V>;
     using S = typename A::S;
     constexpr uint32_t kHalf = sizeof(V) == 16 ? 32768u : 16384u;  // bytes of a mirror box
@@ -1060,6 +1085,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue(pending);
     }
     if (gt == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    QCG_SPAN_END(4, g, gt == 0);
 }
 
 }  // namespace v4
@@ -1084,6 +1110,22 @@ int sm_count() {
 // Slots per launch such that every CTA's contiguous tile range spans <= kDescCap slots
 // (a CTA spans at most slots/grid + 3).
 int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
+// Persistent grid for `tiles` tiles of n slots: min(tiles, SMs). QCG_GRID=bal: the smallest
+// grid with the same number of group-tile rounds (two groups per CTA take alternate tiles),
+// leaving the other SMs to a concurrently queued chunk; measured on C2: 70.84 vs 71.22 ms
+// per solve, but each launch alone 5% slower (fewer SMs' bandwidth), so not the default.
+uint32_t pass_grid(uint32_t tiles, int n, int sms) {
+    static const bool full = [] {
+        const char* e = std::getenv("QCG_GRID");
+        return !(e && std::string(e) == "bal");
+    }();
+    const uint32_t g0 = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+    if (full || g0 == 0) return g0;
+    const uint32_t rounds = (tiles + 2 * g0 - 1) / (2 * g0);
+    const uint32_t g = (tiles + 2 * rounds - 1) / (2 * rounds);
+    // the descriptor cache bounds the slots one CTA's tile range may span
+    return (static_cast<uint32_t>(n) / g + 3 <= static_cast<uint32_t>(v4::kDescCap)) ? g : g0;
+}
 }  // namespace
 
 size_t pass4_smem() { return v4::kSmem; }
@@ -1156,7 +1198,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-            const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+            const uint32_t grid = pass_grid(tiles, n, sms);
             const CUtensorMap tm = state_tensor_map(
                 static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * (fp32 ? 8 : 16),
                 static_cast<uint64_t>(n) << Q, fp32);
@@ -1174,7 +1216,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+        const uint32_t grid = pass_grid(tiles, n, sms);
         if (fp32)
             launch_ex(v4::k_pass_a<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
                       pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles);
@@ -1326,7 +1368,7 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-            const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+            const uint32_t grid = pass_grid(tiles, n, sms);
             P.dims[4] = (1ull << P.geo.hi_bits) * static_cast<cuuint64_t>(n);
             CUtensorMap tm;
             const cuuint32_t es[5] = {1, 1, 1, 1, 1};
@@ -1354,7 +1396,7 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-        const uint32_t grid = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
+        const uint32_t grid = pass_grid(tiles, n, sms);
         static const uint32_t nolev = [] {
             const char* e = std::getenv("QCG_LEVREG");
             return (e && e[0] == '0') ? static_cast<uint32_t>(F_NOLEVREG) : 0u;
@@ -1379,5 +1421,15 @@ extern "C" int qc_trace_read(long long* out, int n) {
     cudaMemcpyToSymbol(v4::g_trace, zero, sizeof(zero));
     return 0;
 }
+extern "C" int qc_trace_read_ctas(unsigned long long* out, int n) {
+    if (n > v4::kTraceMaxCtas * 4) n = v4::kTraceMaxCtas * 4;
+    if (cudaMemcpyFromSymbol(out, v4::g_cta, n * sizeof(unsigned long long)) != cudaSuccess) return 4;
+    static unsigned long long zero[v4::kTraceMaxCtas * 4] = {};
+    cudaMemcpyToSymbol(v4::g_cta, zero, sizeof(zero));
+    return 0;
+}
 #endif
 }  // namespace qcg
+#ifdef QCG_TRACE
+QCG_SPAN_READER(qc_span_read_pass)
+#endif

@@ -116,3 +116,21 @@ def test_c5_sampled_26_qubits(engine):
     e = generate_er(16000, 0.1, 0)
     cfg = dict(qubit_cap=26, top_k=2, layers=1, budget=40, seed=0)
     _check_sampled(engine, ref, 16000, e, 640, [0, 320], **cfg)
+
+
+@pytest.mark.parametrize("n,p", [(1500, 0.05), (2000, 0.1)])
+def test_level_merge_long_chain_top1(engine, n, p):
+    """BASELINE configs[3] K sweep, K=1: every pool holds one class (b, ~b), so only two
+    compatible chains exist and the auto mode picks the level merge over ALL M levels
+    (79 / 106 > the search's 64-level local stacks: the long-window path). Cut,
+    assignment and leaf count against the reference's stock run_pipeline."""
+    from paper_2603_26232_b200 import generate_er
+    ref = _ref()
+    e = generate_er(n, p, 0)
+    cfg = dict(qubit_cap=20, top_k=1, layers=1, budget=4, seed=0)
+    stock = ref.run_pipeline(n, e, workers=CORES, **cfg)
+    rep = engine.run_pipeline(n, e, **cfg)
+    assert rep.subgraphs == stock["subgraphs"] > 64
+    assert rep.cut == stock["cut"]
+    assert rep.assignment == stock["assignment"]
+    assert rep.candidates_evaluated == stock["leaves"]

@@ -59,7 +59,8 @@ def run(workload: str, precision: int, budget: int, max_launches: int):
         val = float(row["Metric Value"].replace(",", ""))
         unit = row.get("Metric Unit", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
-                 "GB": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(unit, 1)
+                 "GB": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9,
+                 "us": 1e-6, "ms": 1e-3}.get(unit, 1)
         d[row["Metric Name"]] = val * scale
     agg = {}
     for (_, k), d in per.items():

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--slots", type=int, default=21)
     ap.add_argument("--layers", type=int, default=1)
     ap.add_argument("--dump", default="")
+    ap.add_argument("--profile", action="store_true")
     a = ap.parse_args()
     lib = pkg.load_library(os.path.join(ROOT, "build", "libqcgpu_trace.so"))
     pkg._LIB = lib
@@ -42,9 +43,18 @@ def main():
     idx = np.arange(a.slots, dtype=np.int32)
     prm = rng.uniform(0.1, 3.0, size=(a.slots, 2 * a.layers))
     eng.eval_batch(graphs, a.layers, idx, prm)
+    if a.profile:  # CUDA-event time of the same launches, for the launch overhead
+        eng.profile(1)
     buf = np.zeros(CTAS * 2 * TILES * EV, np.int64)
     eng.eval_batch(graphs, a.layers, idx, prm)
     lib.qc_trace_read(buf.ctypes.data_as(C.POINTER(C.c_longlong)), C.c_int(buf.size))
+    ctab = np.zeros(1024 * 4, np.uint64)
+    lib.qc_trace_read_ctas(ctab.ctypes.data_as(C.POINTER(C.c_ulonglong)), C.c_int(ctab.size))
+    ctab = ctab.reshape(1024, 4).astype(np.int64)
+    ctab = ctab[ctab[:, 0] > 0]
+    if a.profile:
+        pr = eng.profile_read()
+        eng.profile(False)
     t = buf.reshape(CTAS, 2, TILES, EV)
     out = {"q": a.q, "slots": a.slots, "layers": a.layers, "ctas": []}
     for c in range(CTAS):
@@ -58,6 +68,18 @@ def main():
                             "first_top": int(rows[0][0] - t0) if rows else None,
                             "last_end": int(rows[-1][7] - t0) if rows else None}
         out["ctas"].append(cta)
+    if a.profile:
+        out["event_us"] = {k: round(1e3 * v["ms"] / v["launches"], 2) for k, v in pr.items() if v["launches"]}
+    if len(ctab):
+        t0 = ctab[:, 0].min()
+        ends = np.maximum(ctab[:, 2], ctab[:, 3]) - t0
+        out["launch_ns"] = {
+            "ctas": int(len(ctab)),
+            "entry_spread": int(ctab[:, 0].max() - t0),
+            "prologue_mean": float(np.mean(ctab[:, 1] - ctab[:, 0])),
+            "end_min": int(ends.min()), "end_median": float(np.median(ends)), "end_max": int(ends.max()),
+            "group_end_gap_mean": float(np.mean(np.abs(ctab[:, 2] - ctab[:, 3]))),
+        }
     print(json.dumps(out))
     if a.dump:
         np.save(a.dump, t)
