@@ -358,7 +358,7 @@ __device__ __forceinline__ uint32_t ph5(uint32_t e) {
         return (r << 3) | ((((u >> 1) ^ (r >> 1)) & 3u) << 1) | (u & 1u);
 }
 
-template <typename V>
+template <typename V, bool INIT>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass_a5(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
               int Q, uint32_t flags, uint32_t total_tiles, const __grid_constant__ CUtensorMap tmap) {
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tshift = Q - 12;
     const uint32_t tmask = (1u << tshift) - 1u;
     QCG_CTA(0, tid == 0);
-    const bool init = flags & F_INIT;
+    constexpr bool init = INIT;  // first layer: |+> (no state read)
     const bool wht = flags & F_WHT;
     uint32_t t0;
     int cnt;
@@ -444,13 +444,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int s = k % kStages;
         const uint32_t t = t0 + static_cast<uint32_t>(k);
+        // tile-constant descriptor fields, read once (pd lives in shared memory next to the
+        // stages the rounds write)
         const PD& d = pd[(t >> tshift) - sa];
-        const bool act = init || d.phase || d.mix;
-        const bool use_lev = d.phase && d.lev;
-        const bool lut_sm = use_lev && d.lut_len <= kLutCap;
+        const bool phase = d.phase, mix = d.mix;
+        const bool act = init || phase || mix;
+        const bool use_lev = phase && d.lev;
+        const int lut_len = d.lut_len;
+        const bool lut_sm = use_lev && lut_len <= kLutCap;
+        const V* const glut = reinterpret_cast<const V*>(d.lut);
+        const S amp0 = static_cast<S>(d.amp0);
         if (lut_sm && lut_owner != d.key) {
-            const V* lsrc = reinterpret_cast<const V*>(d.lut);
-            for (int i = static_cast<int>(gt); i < d.lut_len; i += kGT) slut[i] = lsrc[i];
+            // the init layer stages amp0 * lut (the same cmul each amplitude would do)
+            for (int i = static_cast<int>(gt); i < lut_len; i += kGT) {
+                const V l = glut[i];
+                slut[i] = init ? A::cmul(A::mk(amp0, S(0)), l) : l;
+            }
             lut_owner = d.key;
             grp_sync(g);
         }
@@ -467,13 +476,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t base = (t & tmask) << 12;
         V* st = reinterpret_cast<V*>(sm + s * kStageAmpBytes);
         const double c = d.c, sn = d.s;
-        const bool mix = d.mix;
         V a[16];
-        {
+        // round 0: phase + bits 0-3. Two instantiations so the staged-LUT reads compile to
+        // LDS (a pointer that may be shared or global compiles to generic loads, which wait
+        // on the long scoreboard); `pre`: the staged LUT already holds amp0 * lut.
+        auto round0 = [&](const V* __restrict__ lutp, bool pre) {
             const uint4* lv = reinterpret_cast<const uint4*>(sm + kOffLev + s * 8192u) + gt * 2u;
-            const V* lutp = lut_sm ? slut : reinterpret_cast<const V*>(d.lut);
-            const double amp0 = d.amp0;
-            const bool phase = d.phase;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
@@ -481,15 +489,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int jj = 0; jj < 8; ++jj) {
                     const int j = h * 8 + jj;
                     const uint32_t e = gt * 16u + j;
-                    V v = init ? A::mk(static_cast<S>(amp0), S(0)) : st[ph5<V>(e)];
-                    if (phase) {
-                        if (use_lev) {
-                            const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
-                                                : (jj >> 1) == 2 ? l4.z : l4.w;
-                            v = A::cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
-                        } else {
-                            v = phase_frac<V>(v, d.gamma, d.val[base + e]);
-                        }
+                    V v;
+                    if (use_lev) {
+                        const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
+                                            : (jj >> 1) == 2 ? l4.z : l4.w;
+                        const V l = lutp[(word >> ((jj & 1) * 16)) & 0xffffu];
+                        v = init ? (pre ? l : A::cmul(A::mk(amp0, S(0)), l)) : A::cmul(st[ph5<V>(e)], l);
+                    } else {
+                        v = init ? A::mk(amp0, S(0)) : st[ph5<V>(e)];
+                        if (phase) v = phase_frac<V>(v, d.gamma, d.val[base + e]);
                     }
                     a[j] = v;
                 }
@@ -497,7 +505,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[ph5<V>(gt * 16u + j)] = a[j];
-        }
+        };
+        if (lut_sm)
+            round0(slut, init);
+        else
+            round0(glut, false);
         QCG_TR(k, 3);
         __syncwarp();  // round 1 reads only what its own half-warp wrote (e>>8 = gt>>4)
         {
@@ -1179,7 +1191,9 @@ template <typename V>
 void a5_attr() {
     static PerDeviceOnce attr;
     attr.run([] {
-        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kSmem + 1024)));
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(v4::kSmem + 1024)));
     });
 }
@@ -1202,11 +1216,15 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
             const CUtensorMap tm = state_tensor_map(
                 static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * (fp32 ? 8 : 16),
                 static_cast<uint64_t>(n) << Q, fp32);
+            const bool init = flags & F_INIT;
+            auto* kern = fp32 ? (init ? v4::k_pass_a5<float2, true> : v4::k_pass_a5<float2, false>)
+                              : nullptr;
+            auto* kern64 = init ? v4::k_pass_a5<double2, true> : v4::k_pass_a5<double2, false>;
             if (fp32)
-                launch_ex(v4::k_pass_a5<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
+                launch_ex(kern, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
                           pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
             else
-                launch_ex(v4::k_pass_a5<double2>, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
+                launch_ex(kern64, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
                           pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
             ++launches;
         }
