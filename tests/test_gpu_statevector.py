@@ -255,3 +255,82 @@ def test_cost_table_matches_reference(engine, oracle, case):
     assert gint == wint == (case in ("er20", "weighted_int18"))
     assert gmax == wmax
     assert np.array_equal(got, want)
+
+
+def _blocked_sum_ref(f):
+    """statevector.hpp:48-65 blocked_sum: sequential sums over 4096-blocks, then the block
+    partials in order (np.add.accumulate is strictly left to right in float64)."""
+    parts = [np.add.accumulate(np.concatenate(([0.0], f[i:i + 4096])))[-1] for i in range(0, len(f), 4096)]
+    return np.add.accumulate(np.concatenate(([0.0], parts)))[-1]
+
+
+@pytest.mark.parametrize("q,kind", [(13, "ties"), (14, "range"), (15, "crossings"), (16, "mixed"),
+                                    (14, "zeros")])
+def test_blocked_sum_adversarial(engine, q, kind):
+    """The segmented exact block sum (k_blocksum_seg) against the sequential reference on
+    inputs built to break its fast path: exact ties at acc's half-ulp (1 + 2^-53 rounds to
+    even), a 2^-60..2^10 dynamic range, values that cross a binade every few terms, runs of
+    zeros and subnormal-adjacent magnitudes. |a|^2 = a.x^2 + a.y^2 is formed exactly as the
+    kernel forms it, then summed in the reference's order."""
+    rng = np.random.default_rng(q)
+    n = 1 << q
+    if kind == "ties":  # each block: 1.0, then 2^-53 (ties at acc's half-ulp) and 5 * 2^-54
+        re = np.full(n, 2.0 ** -27)
+        im = np.where(rng.random(n) < 0.6, 2.0 ** -27, 2.0 ** -26)
+        re[::4096] = 1.0
+        im[::4096] = 0.0
+    elif kind == "range":
+        re = np.ldexp(rng.random(n) + 0.5, rng.integers(-30, 5, n))
+        im = np.ldexp(rng.random(n) + 0.5, rng.integers(-30, 5, n))
+    elif kind == "crossings":  # geometric growth: the running sum doubles every few terms
+        k = np.arange(n) % 4096
+        re = np.sqrt(np.ldexp(1.0, (k // 3) % 40 - 20)) * (1 + rng.random(n) * 1e-3)
+        im = np.zeros(n)
+    elif kind == "zeros":
+        re = rng.standard_normal(n)
+        im = rng.standard_normal(n)
+        re[rng.random(n) < 0.7] = 0.0
+        im[re == 0.0] = 0.0
+        re[:5000] = 0.0
+        im[:5000] = 0.0
+    else:
+        re = rng.standard_normal(n) * np.ldexp(1.0, rng.integers(-8, 8, n))
+        im = rng.standard_normal(n)
+        im[rng.random(n) < 0.1] = 0.0
+    a = (re + 1j * im).astype(np.complex128)
+    f = a.real * a.real + a.imag * a.imag  # two rounded products, one rounded add
+    got = engine.norm_sq(a)
+    want = _blocked_sum_ref(f)
+    assert got == want, (kind, got, want)
+
+
+@pytest.mark.parametrize("q,kind", [(24, "ties"), (24, "range"), (25, "crossings"), (24, "smooth")])
+def test_partial_sum_adversarial(engine, q, kind):
+    """The in-order sum over the block partials (statevector.hpp:61-62; 4096 partials at
+    q=24, 8192 at q=25 = two 4096-chunks carried) runs the segmented exact sum. Each block
+    holds one nonzero amplitude at its first index, so its partial is exactly that f value
+    and the partial sequence is chosen freely: ties at acc's half-ulp, a wide dynamic range,
+    binade crossings every few partials, and smooth data (the fast path)."""
+    rng = np.random.default_rng(q + len(kind))
+    n, nbl = 1 << q, 1 << (q - 12)
+    if kind == "ties":
+        x = np.full(nbl, 2.0 ** -27)
+        y = np.where(rng.random(nbl) < 0.6, 2.0 ** -27, 2.0 ** -26)
+        x[::512] = 1.0
+        y[::512] = 0.0
+    elif kind == "range":
+        x = np.ldexp(rng.random(nbl) + 0.5, rng.integers(-40, 10, nbl))
+        y = np.ldexp(rng.random(nbl) + 0.5, rng.integers(-40, 10, nbl))
+    elif kind == "crossings":
+        k = np.arange(nbl)
+        x = np.sqrt(np.ldexp(1.0, (k // 2) % 50 - 25)) * (1 + rng.random(nbl) * 1e-3)
+        y = np.zeros(nbl)
+    else:
+        x = 1e-3 * (1 + rng.random(nbl))
+        y = 1e-3 * rng.random(nbl)
+    a = np.zeros(n, np.complex128)
+    a[:: 4096] = x + 1j * y
+    v = x * x + y * y
+    want = np.add.accumulate(np.concatenate(([0.0], v)))[-1]
+    got = engine.norm_sq(a)
+    assert got == want, (kind, got, want)
