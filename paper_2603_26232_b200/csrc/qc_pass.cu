@@ -554,6 +554,216 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// pass A, split-buffer variant (fp64 default): one input stage PER GROUP plus one output
+// buffer SHARED by the two groups, instead of a three-stage in/out ring.
+//
+// Why. In k_pass_a5 the tile's stage is also its output staging, so the stage can be
+// refilled only after the 64 KB bulk store has read it (~2.9k clk at the SM's share of
+// HBM), and only the thread that issued a bulk store can wait for it: the group's elected
+// lane blocked ~2.7k clk per tile at the top of its next tile and the whole group then
+// waited for that warp at the round-2 barrier (tools/trace_pass.py). Here a group's input
+// stage is free as soon as round 2 has loaded it into registers, so the elected lane
+// refills it with the group's next tile right then, with nothing to wait for. The results
+// go to OUT, which the two groups use alternately (tile n, n+1, ... in local order): the
+// writer of tile n waits on `out_free` for the release of tile n-1, and a group releases
+// its last write after round 0 of its next tile, when the store has long read OUT (its
+// wait_group.read returns at once). Shared memory: 2 x 64 KB in + 64 KB out + 2 x 8 KB of
+// cut levels + two 480-entry phase LUTs (C3's weighted LUTs fit) + descriptors.
+// ---------------------------------------------------------------------------
+constexpr int kLutCap7 = 480;
+constexpr uint32_t kA7OffOut = 2u * kStageAmpBytes;
+constexpr uint32_t kA7OffLev = 3u * kStageAmpBytes;
+constexpr uint32_t kA7OffLut = kA7OffLev + 2u * 8192u;
+constexpr uint32_t kA7OffBar = kA7OffLut + 2u * kLutCap7 * 16u;  // full[2], out_free
+constexpr uint32_t kA7OffDesc = kA7OffBar + 32u;
+constexpr uint32_t kA7Smem = kA7OffDesc + kDescCap * sizeof(PD);
+static_assert(kA7Smem + 1024 <= 232448, "a7 shared memory budget");
+
+template <typename V, bool INIT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_pass_a7(const SlotDesc* __restrict__ slots, const LayerParam* __restrict__ lp, int layer,
+              int Q, uint32_t flags, uint32_t total_tiles, const __grid_constant__ CUtensorMap tmap) {
+    QCG_SPAN_BEGIN();
+    using A = Amp<V>;
+    using S = typename A::S;
+    constexpr uint32_t kTileBytes = 4096u * sizeof(V);
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((1024u - (su32(sm_raw) & 1023u)) & 1023u);  // TMA 128B swizzle
+    const uint32_t tid = threadIdx.x, g = tid / kGT, gt = tid % kGT;
+    const int tshift = Q - 12;
+    const uint32_t tmask = (1u << tshift) - 1u;
+    QCG_CTA(0, tid == 0);
+    constexpr bool init = INIT;
+    const bool wht = flags & F_WHT;
+    uint32_t t0;
+    int cnt;
+    tile_range(total_tiles, t0, cnt);
+    if (cnt <= 0) return;
+    const uint32_t sa = t0 >> tshift;
+    PD* pd = reinterpret_cast<PD*>(sm + kA7OffDesc);
+    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    const uint32_t full = su32(sm + kA7OffBar) + g * 8u;  // this group's input barrier
+    const uint32_t ofree = su32(sm + kA7OffBar) + 16u;
+    if (tid < 2) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(sm + kA7OffBar) + tid * 8u) : "memory");
+    if (tid == 2) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(sm + kA7OffBar) + 16u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();
+
+    unsigned char* in = sm + g * kStageAmpBytes;
+    unsigned char* lev = sm + kA7OffLev + g * 8192u;
+    // elected lane: load local tile k (one of this group's) into the group's stage
+    auto issue = [&](int k) {
+        if (k >= cnt || gt != 0) return;
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool lv = d.phase && d.lev;
+        if (init || d.phase || d.mix) {
+            const uint32_t bytes = (init ? 0u : kTileBytes) + (lv ? 8192u : 0u);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(full), "r"(bytes)
+                         : "memory");
+            if (!init)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                    "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(su32(in)),
+                    "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(t << 8), "r"(0), "r"(full)
+                    : "memory");
+            if (lv)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 8192, [%2];\n" ::"r"(
+                        su32(lev)),
+                    "l"(d.lev + ((t & tmask) << 12)), "r"(full)
+                    : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(full) : "memory");
+        }
+    };
+    // release this group's last OUT write (its store has read OUT by now)
+    bool pending = false;
+    auto release = [&] {
+        if (pending) {
+            if (gt == 0) {
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                bar_arrive(ofree);
+            }
+            pending = false;
+        }
+    };
+    issue(static_cast<int>(g));
+
+    QCG_CTA(1, tid == 0);
+    V* slut = reinterpret_cast<V*>(sm + kA7OffLut) + g * kLutCap7;
+    V* out = reinterpret_cast<V*>(sm + kA7OffOut);
+    int lut_owner = -1;
+    uint32_t it = 0;  // this group's tile count (input barrier phase)
+    for (int k = static_cast<int>(g); k < cnt; k += 2, ++it) {
+        QCG_TR(k, 0);
+        const uint32_t t = t0 + static_cast<uint32_t>(k);
+        const PD& d = pd[(t >> tshift) - sa];
+        const bool phase = d.phase, mix = d.mix;
+        const bool act = init || phase || mix;
+        const bool use_lev = phase && d.lev;
+        const int lut_len = d.lut_len;
+        const bool lut_sm = use_lev && lut_len <= kLutCap7;
+        const V* const glut = reinterpret_cast<const V*>(d.lut);
+        const S amp0 = static_cast<S>(d.amp0);
+        if (lut_sm && lut_owner != d.key) {
+            for (int i = static_cast<int>(gt); i < lut_len; i += kGT) {
+                const V l = glut[i];
+                slut[i] = init ? A::cmul(A::mk(amp0, S(0)), l) : l;
+            }
+            lut_owner = d.key;
+            grp_sync(g);
+        }
+        QCG_TR(k, 1);
+        bar_wait(full, it & 1u);
+        QCG_TR(k, 2);
+        if (!act) {  // identity layer: memory already holds the result; keep OUT's turn order
+            release();
+            if (k > 0) bar_wait(ofree, static_cast<uint32_t>((k - 1) & 1));
+            grp_sync(g);
+            if (gt == 0) bar_arrive(ofree);
+            issue(k + 2);
+            continue;
+        }
+        const uint32_t base = (t & tmask) << 12;
+        V* st = reinterpret_cast<V*>(in);
+        const double c = d.c, sn = d.s;
+        V a[16];
+        auto round0 = [&](const V* __restrict__ lutp, bool pre) {
+            const uint4* lv = reinterpret_cast<const uint4*>(lev) + gt * 2u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = h * 8 + jj;
+                    const uint32_t e = gt * 16u + j;
+                    V v;
+                    if (use_lev) {
+                        const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
+                                            : (jj >> 1) == 2 ? l4.z : l4.w;
+                        const V l = lutp[(word >> ((jj & 1) * 16)) & 0xffffu];
+                        v = init ? (pre ? l : A::cmul(A::mk(amp0, S(0)), l)) : A::cmul(st[ph5<V>(e)], l);
+                    } else {
+                        v = init ? A::mk(amp0, S(0)) : st[ph5<V>(e)];
+                        if (phase) v = phase_frac<V>(v, d.gamma, d.val[base + e]);
+                    }
+                    a[j] = v;
+                }
+            }
+            if (mix) mix4<V>(a, c, sn, wht);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[ph5<V>(gt * 16u + j)] = a[j];
+        };
+        if (lut_sm)
+            round0(slut, init);
+        else
+            round0(glut, false);
+        QCG_TR(k, 3);
+        release();     // the previous write's store has read OUT long ago
+        __syncwarp();  // round 1 reads only what its own half-warp wrote (e>>8 = gt>>4)
+        {
+            const uint32_t r = ((gt >> 4) << 8) | (gt & 15u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>(r | (j << 4))];
+            if (mix) mix4<V>(a, c, sn, wht);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) st[ph5<V>(r | (j << 4))] = a[j];
+        }
+        QCG_TR(k, 4);
+        grp_sync(g);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = st[ph5<V>((j << 8) | gt)];
+        grp_sync(g);   // the group's stage and levels are consumed: load its next tile now
+        issue(k + 2);
+        QCG_TR(k, 5);
+        if (mix) mix4<V>(a, c, sn, wht);
+        // OUT's turn: tile k-1 (the other group) must have released it
+        if (k > 0) bar_wait(ofree, static_cast<uint32_t>((k - 1) & 1));
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[(j << 8) | gt] = a[j];  // linear, conflict-free
+        QCG_TR(k, 6);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        grp_sync(g);
+        QCG_TR(k, 7);
+        if (gt == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                             reinterpret_cast<V*>(d.state) + base),
+                         "r"(su32(out)), "r"(kTileBytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        }
+        pending = true;
+    }
+    release();
+    if (gt == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    QCG_CTA(2 + g, gt == 0);
+    QCG_SPAN_END(1, g, gt == 0);
+}
+
+// ---------------------------------------------------------------------------
 // pass B: tile = 8 contiguous amps (column bits 0-2) x 9 gathered tile bits (RX targets
 // >= 12, then the mirror pseudo-bit whose mask is every stored bit, then no-op pads).
 // Tile index e = w | gb << 3 (gb: 9 gather bits); global index = x ^ hx(gb) where
@@ -1178,6 +1388,14 @@ CUtensorMap state_tensor_map(const void* base, uint64_t amps, bool fp32 = false)
 // TMA pass A: default for fp64, and for fp32 at Q >= 21 (fp32 per launch with 2-4 slots:
 // q=24 161.9 -> 146.1 us, q=26 313 -> 276; q=20 60.6 -> 58.8 but the C2 bench is 1% slower;
 // the C3/C5 fp32 solves are unchanged); QCG_PASS_A=v4|tma forces one kernel
+// fp64 TMA pass A kernel: the split-buffer a7 (default) or the ring a5 (QCG_PASS_A=a5)
+bool use_a7() {
+    static const bool a7 = [] {
+        const char* e = std::getenv("QCG_PASS_A");
+        return !(e && std::string(e) == "a5");
+    }();
+    return a7;
+}
 bool tma_pass_a(bool fp32, int Q) {
     static const int mode = [] {
         const char* e = std::getenv("QCG_PASS_A");
@@ -1195,6 +1413,10 @@ void a5_attr() {
                                      static_cast<int>(v4::kSmem + 1024)));
         QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a5<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(v4::kSmem + 1024)));
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a7<V, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kA7Smem + 1024)));
+        QC_CUDA(cudaFuncSetAttribute(v4::k_pass_a7<V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(v4::kA7Smem + 1024)));
     });
 }
 }  // namespace
@@ -1223,6 +1445,10 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
             if (fp32)
                 launch_ex(kern, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
                           pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
+            else if (use_a7())
+                launch_ex(init ? v4::k_pass_a7<double2, true> : v4::k_pass_a7<double2, false>, dim3(grid),
+                          dim3(v4::kThreads), v4::kA7Smem + 1024, stream, pdl || s0 > 0, d_slots + s0, d_lp,
+                          layer, Q, flags, tiles, tm);
             else
                 launch_ex(kern64, dim3(grid), dim3(v4::kThreads), v4::kSmem + 1024, stream,
                           pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles, tm);
