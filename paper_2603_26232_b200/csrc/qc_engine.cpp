@@ -145,7 +145,7 @@ std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool 
         off[i] = bytes;
         if (!unit_cost) {
             const size_t entries = size_t{1} << d.Q;
-            bytes += (d.integral ? 2 : 8) * entries;
+            bytes += (d.integral ? 2 : 10) * entries;  // non-integral: values + index levels
             bytes = (bytes + 255) & ~size_t{255};
         }
         eoff[i] = ebytes;
@@ -176,6 +176,31 @@ std::vector<DevGraph> qc_engine::prepare(const std::vector<HostGraph>& hg, bool 
                                   reinterpret_cast<double*>(de + m * 8), static_cast<int>(m), d.Q,
                                   d.integral, d.lev, d.val, stream);
         prof.end(stream);
+    }
+    // non-integral tables: exact phases through a LUT over the distinct values (qc_frac.cu)
+    int* d_count = nullptr;
+    for (size_t i = 0; i < hg.size(); ++i) {
+        DevGraph& d = dg[i];
+        if (d.integral) continue;
+        const uint32_t N = uint32_t{1} << d.Q;
+        void* scratch = distinct.get(distinct_scratch_bytes(N) + 64);
+        d_count = reinterpret_cast<int*>(static_cast<char*>(scratch) + distinct_scratch_bytes(N));
+        const unsigned long long* uniq = launch_distinct(d.val, N, scratch, d_count, stream);
+        int D = 0;
+        QC_CUDA(cudaMemcpyAsync(&D, d_count, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        QC_CUDA(cudaStreamSynchronize(stream));
+        d2h += sizeof(int);
+        if (D < 1 || D > kMaxDistinct) continue;  // device sincos (within 1e-10)
+        std::vector<unsigned long long> bits(static_cast<size_t>(D));
+        QC_CUDA(cudaMemcpyAsync(bits.data(), uniq, bits.size() * 8, cudaMemcpyDeviceToHost, stream));
+        d2h += bits.size() * 8;
+        d.lev = reinterpret_cast<uint16_t*>(base + off[i] + size_t{8} * N);
+        launch_index_of(d.val, N, uniq, D, d.lev, stream);
+        ++launches;
+        QC_CUDA(cudaStreamSynchronize(stream));
+        d.fvals.resize(bits.size());
+        std::memcpy(d.fvals.data(), bits.data(), bits.size() * 8);
+        d.lut_len = D;
     }
     // the host staging buffer is reused by the next upload: wait for this copy
     QC_CUDA(cudaStreamSynchronize(stream));
@@ -265,7 +290,7 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     size_t lut_total = 0;
     for (int k = 0; k < n; ++k) {
         const DevGraph& d = dg[static_cast<size_t>(pts[k].g)];
-        if (d.integral && !d.unit_cost)
+        if (d.lev && !d.unit_cost)
             for (int l = 0; l < p; ++l)
                 if (pts[k].x[l] != 0.0) lut_total += static_cast<size_t>(d.lut_len);
     }
@@ -301,8 +326,11 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
         SlotDesc& s = hs[k];
         s.state = reinterpret_cast<double2*>(st + static_cast<size_t>(k) * N * ab);
         s.fbuf = fb ? reinterpret_cast<double*>(fb + static_cast<size_t>(k) * N * fbb) : nullptr;
-        s.lev = dgk.unit_cost ? nullptr : dgk.lev;
+        // integral: lev = plev = cut levels; fractional: val = cut values, plev = the index
+        // of each among the distinct values (null: device sincos), lev = null
+        s.lev = (dgk.unit_cost || !dgk.integral) ? nullptr : dgk.lev;
         s.val = dgk.unit_cost ? nullptr : dgk.val;
+        s.plev = dgk.unit_cost ? nullptr : dgk.lev;
         s.amp0 = amp0;
         s.layer_base = k * p;
         s.pad = 0;
@@ -321,19 +349,22 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             L.lut = nullptr;
             L.lut_len = 0;
             L.pad = 0;
-            if (L.phase && dgk.integral && !dgk.unit_cost) {
-                // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c)
+            if (L.phase && dgk.lev && !dgk.unit_cost) {
+                // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c); non-integral
+                // tables (:162-164): std::polar(1.0, -gamma * val) for each distinct val
+                const double* fv = dgk.fvals.empty() ? nullptr : dgk.fvals.data();
+                auto arg = [&](int c) { return -gamma * (fv ? fv[c] : static_cast<double>(c)); };
                 if (fp32) {
                     float* dst = reinterpret_cast<float*>(h + o_lut) + 2 * lut_pos;
                     for (int c = 0; c < dgk.lut_len; ++c) {
-                        const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
+                        const std::complex<double> z = std::polar(1.0, arg(c));
                         dst[2 * c] = static_cast<float>(z.real());
                         dst[2 * c + 1] = static_cast<float>(z.imag());
                     }
                 } else {
                     double* dst = hlut + 2 * lut_pos;
                     for (int c = 0; c < dgk.lut_len; ++c) {
-                        const std::complex<double> z = std::polar(1.0, -gamma * static_cast<double>(c));
+                        const std::complex<double> z = std::polar(1.0, arg(c));
                         dst[2 * c] = z.real();
                         dst[2 * c + 1] = z.imag();
                     }

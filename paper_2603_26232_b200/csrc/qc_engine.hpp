@@ -49,8 +49,9 @@ struct DevGraph {
     bool integral = true;
     bool unit_cost = false;  // norm_sq: cost 1 everywhere
     int lut_len = 0;
-    uint16_t* lev = nullptr;
-    double* val = nullptr;
+    uint16_t* lev = nullptr;   // integral: cut levels; else (when set) indices into fvals
+    double* val = nullptr;     // non-integral: C(z) in edge order (the expectation's cost)
+    std::vector<double> fvals; // non-integral: distinct values of val (host), the phase LUT's arguments
 };
 
 struct EvalPoint {
@@ -114,6 +115,7 @@ struct qc_engine {
     uint64_t mem_budget = 0;
     mutable size_t auto_budget = 0;  // 60% of the free HBM seen at first use
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
+    qcg::DevBuf distinct;  // scratch of the non-integral tables' distinct-value search
     qcg::HostBuf hstage, hout;
     qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
     qcg::DeviceArena merge_arena;                           // merge scratch, reused

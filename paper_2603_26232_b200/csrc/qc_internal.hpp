@@ -81,8 +81,11 @@ constexpr int kBlock = 4096;   // statevector.hpp:53 blocked_sum block
 struct SlotDesc {
     double2* state;        // 2^Q stored amplitudes
     double* fbuf;          // 2^Q per-amplitude expectation terms (scratch)
-    const uint16_t* lev;   // integral cut levels, 2^Q entries (or null)
+    const uint16_t* lev;   // integral cut levels, 2^Q entries (or null): the expectation's cost
     const double* val;     // fractional cut values, 2^Q entries (or null)
+    const uint16_t* plev;  // phase LUT index per z: the integral levels, or for a fractional
+                           // table the index of val[z] among its distinct values (qc_frac.cu);
+                           // null: device sincos phases
     double amp0;           // 1/sqrt(2^q)
     int32_t layer_base;    // first LayerParam of this slot
     int32_t pad;
@@ -213,6 +216,13 @@ struct ChainStats {
 // Launchers (qc_kernels.cu). All asynchronous on `stream`; return #kernels launched.
 int launch_levels(const uint32_t* d_eu, const uint32_t* d_ev, const double* d_ew, int m,
                   int Q, bool integral, uint16_t* d_lev, double* d_val, cudaStream_t stream);
+// qc_frac.cu: distinct values of a non-integral cost table (exact phases via a host LUT)
+size_t distinct_scratch_bytes(uint32_t N);
+const unsigned long long* launch_distinct(const double* d_val, uint32_t N, void* scratch, int* d_count,
+                                          cudaStream_t st);
+void launch_index_of(const double* d_val, uint32_t N, const unsigned long long* d_uniq, int D, uint16_t* d_lev,
+                     cudaStream_t st);
+constexpr int kMaxDistinct = 65535;  // uint16 level indices
 // d_tickets: n_slots zero-initialised counters (left zeroed on return).
 // d_fbuf: the f buffer of slot 0 of this launch (slots contiguous, 2^Q doubles each).
 int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerParam* d_lp,

@@ -66,7 +66,7 @@ __device__ __forceinline__ double cost_of(const SlotDesc& S, uint32_t g) {
 // statevector.hpp:154-164: lut[lev] (integral) or std::polar(1, -gamma*val) (fractional)
 __device__ __forceinline__ double2 phase_rn(double2 a, const SlotDesc& S, const LayerParam& L,
                                             uint32_t g) {
-    if (S.lev) return cmul_rn(a, L.lut[S.lev[g]]);
+    if (S.plev) return cmul_rn(a, L.lut[S.plev[g]]);
     double sn, cs;
     sincos(__dmul_rn(-L.gamma, S.val[g]), &sn, &cs);
     return cmul_rn(a, make_double2(cs, sn));
@@ -256,8 +256,8 @@ __global__ void __launch_bounds__(kOnchipThreads) k_onchip_f32(const SlotDesc* _
         if (L.phase) {
             const float2* lut = reinterpret_cast<const float2*>(L.lut);
             for (uint32_t e = tid; e < N; e += kOnchipThreads) {
-                if (S.lev) {
-                    sa[e] = A::cmul(sa[e], lut[S.lev[e]]);
+                if (S.plev) {
+                    sa[e] = A::cmul(sa[e], lut[S.plev[e]]);
                 } else {
                     double s_, c_;
                     sincos(-L.gamma * S.val[e], &s_, &c_);
@@ -428,9 +428,9 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_pass_low(const SlotDesc* __
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = st[k * kPassThreads + tid];
     }
-    const bool use_lev = L.phase && S.lev;
+    const bool use_lev = L.phase && S.plev;
     uint4 lv4 = make_uint4(0, 0, 0, 0);
-    if (use_lev) lv4 = *reinterpret_cast<const uint4*>(S.lev + base + tid * 8u);
+    if (use_lev) lv4 = *reinterpret_cast<const uint4*>(S.plev + base + tid * 8u);
     const bool lut_sm = use_lev && L.lut_len <= kLutSmem;
     if (lut_sm)
         for (int i = tid; i < L.lut_len; i += kPassThreads) slut[i] = L.lut[i];

@@ -136,6 +136,9 @@ __device__ __forceinline__ void tile_range(uint32_t total, uint32_t& t0, int& cn
 }
 
 // Slot range of this CTA's tiles -> descriptor cache (caller guarantees it fits).
+// PHASE: the phase passes (pass A) read the phase-LUT index levels (SlotDesc::plev), the
+// f passes (pass B) the cost levels (SlotDesc::lev)
+template <bool PHASE = false>
 __device__ __forceinline__ void load_descs(PD* pd, const SlotDesc* __restrict__ slots,
                                            const LayerParam* __restrict__ lp, int layer,
                                            uint32_t sa, uint32_t n) {
@@ -145,7 +148,7 @@ __device__ __forceinline__ void load_descs(PD* pd, const SlotDesc* __restrict__ 
         PD d;
         d.state = S.state;
         d.fbuf = S.fbuf;
-        d.lev = S.lev;
+        d.lev = PHASE ? S.plev : S.lev;
         d.val = S.val;
         d.lut = L.lut;
         d.amp0 = S.amp0;
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (cnt <= 0) return;
     const uint32_t sa = t0 >> tshift;
     PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
-    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    load_descs<true>(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
     ring_init(sm);
     __syncthreads();
     pdl_trigger();
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (cnt <= 0) return;
     const uint32_t sa = t0 >> tshift;
     PD* pd = reinterpret_cast<PD*>(sm + kOffDesc);
-    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    load_descs<true>(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
     const uint32_t bar0 = su32(sm + kOffBar);
     volatile int* tag = reinterpret_cast<volatile int*>(sm + kOffTag);
     if (tid < kStages) {
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (cnt <= 0) return;
     const uint32_t sa = t0 >> tshift;
     PD* pd = reinterpret_cast<PD*>(sm + kA7OffDesc);
-    load_descs(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
+    load_descs<true>(pd, slots, lp, layer, sa, ((t0 + cnt - 1) >> tshift) - sa + 1);
     const uint32_t full = su32(sm + kA7OffBar) + g * 8u;  // this group's input barrier
     const uint32_t ofree = su32(sm + kA7OffBar) + 16u;
     if (tid < 2) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(sm + kA7OffBar) + tid * 8u) : "memory");

@@ -98,6 +98,20 @@ def test_c3_sampled_full_budget(engine):
     _check_sampled(engine, ref, 1000, e, 44, [0, 21, 43], **cfg)
 
 
+@pytest.mark.parametrize("scale", [4.0, 10.0])
+def test_c3_fractional_variant_sampled(engine, scale):
+    """Config 3 with fractional weights U{1..10}/4 (dyadic) and U{1..10}/10 (decimal): the
+    non-integral cost tables (statevector.hpp:162-164, per-amplitude std::polar in the
+    reference). Two 24-qubit pieces and the tail, NM budget 60: every SolveResult field
+    identical to the reference build's."""
+    from paper_2603_26232_b200 import generate_regular
+    ref = _ref()
+    e = generate_regular(1000, 3, 0, 1, 10).copy()
+    e["w"] = e["w"] / scale
+    cfg = dict(qubit_cap=24, top_k=2, layers=1, budget=60, seed=0)
+    _check_sampled(engine, ref, 1000, e, 44, [0, 21, 43], **cfg)
+
+
 def test_c4_sampled_full_budget(engine):
     """Config 4: ER(10000, 0.1, 0), cap 20 -> 527 pieces; four pieces incl. the 6-vertex
     tail, budget 200, K=8 (the top of the config-4 K sweep)."""

@@ -147,24 +147,56 @@ def test_duplicate_edges_rejected_like_add_edge(engine, n):
         assert integral and mx == 2.0
 
 
-@pytest.mark.parametrize("q,layers", [(10, 1), (14, 2), (20, 2), (22, 1), (24, 1)])
-def test_fractional_weights_within_tolerance(engine, oracle, q, layers):
-    """Non-integral weights take statevector.hpp:162-164 (per-amplitude std::polar). The
-    device evaluates sin/cos itself; glibc's sin/cos are not correctly rounded (~0.13% of
-    arguments differ from the correctly rounded value by 1 ulp), so this path is held to
-    the north-star fp64 tolerance (1e-10 relative), not to bit equality."""
-    rng = np.random.default_rng(q)
-    e = oracle.generate_er(q, 0.3, q).copy()
-    e["w"] = rng.uniform(0.1, 1.1, len(e))
+def _frac_graph(oracle, q, kind, seed):
+    rng = np.random.default_rng(seed)
+    e = oracle.generate_er(q, 0.3, seed).copy()
+    if kind == "real":
+        e["w"] = rng.uniform(0.1, 1.1, len(e))
+    elif kind == "quarter":  # dyadic: every cut value exact, few distinct
+        e["w"] = rng.integers(1, 11, len(e)) / 4.0
+    elif kind == "tenth":  # decimal: edge-order rounding, a few thousand distinct values
+        e["w"] = rng.integers(1, 11, len(e)) / 10.0
+    else:  # "heavy": integral but total > 65535 (statevector.hpp:89, the values path)
+        e["w"] = rng.integers(1000, 9000, len(e)).astype(np.float64)
+    return e
+
+
+def _ansatz_both(engine, oracle, q, e, layers, seed):
+    rng = np.random.default_rng(seed + 7)
     g = rng.uniform(0.2, np.pi, layers)
     b = rng.uniform(0.2, np.pi, layers)
     a0, x0 = oracle.run_ansatz(q, e, g, b, threads=max(1, min(32, __import__("os").cpu_count() or 1)))
     a1, x1 = engine.run_ansatz(q, e, g, b)
+    got = engine.eval_batch([(q, e)], layers, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
+    return a0, x0, a1, x1, got[0]
+
+
+@pytest.mark.parametrize("q,layers,kind", [(10, 1, "real"), (14, 2, "real"), (17, 2, "real"),
+                                           (20, 2, "quarter"), (20, 1, "tenth"), (22, 1, "quarter"),
+                                           (24, 1, "tenth"), (18, 2, "heavy")])
+def test_fractional_weights_bit_exact(engine, oracle, q, layers, kind):
+    """Non-integral tables take statevector.hpp:162-164: amps[z] *= std::polar(1, -gamma *
+    val[z]) with glibc's sin/cos. The engine finds the table's distinct values on the device,
+    the host evaluates std::polar for each (the reference's own operation and libm), and the
+    passes apply them through the LUT path; the expectation reads the fp64 values. Every
+    table with <= 65,535 distinct values is bit-exact: all tables up to 17 qubits, dyadic
+    and decimal weights, integral tables whose total exceeds 65,535."""
+    e = _frac_graph(oracle, q, kind, q)
+    a0, x0, a1, x1, xe = _ansatz_both(engine, oracle, q, e, layers, q)
+    assert np.array_equal(a1, a0)
+    assert x1 == x0 and xe == x0
+
+
+@pytest.mark.parametrize("q,layers", [(20, 2), (22, 1)])
+def test_fractional_weights_within_tolerance(engine, oracle, q, layers):
+    """Random real weights on 20+ qubits give more than 65,535 distinct cut values: the
+    device evaluates sin/cos itself (glibc's are not correctly rounded in ~0.13% of
+    arguments), held to the north-star fp64 tolerance (1e-10 relative)."""
+    e = _frac_graph(oracle, q, "real", q)
+    a0, x0, a1, x1, xe = _ansatz_both(engine, oracle, q, e, layers, q)
     assert abs(x1 - x0) <= 1e-10 * abs(x0)
     assert np.max(np.abs(a1 - a0)) <= 1e-10 * np.max(np.abs(a0))
-    # the half-state eval path (value-table f in the last pass, TMA kernels at q >= 22)
-    got = engine.eval_batch([(q, e)], layers, np.zeros(1, np.int32), np.concatenate([g, b])[None, :])
-    assert abs(got[0] - x0) <= 1e-10 * abs(x0)
+    assert abs(xe - x0) <= 1e-10 * abs(x0)
 
 
 @pytest.mark.parametrize("q", [14, 20])
