@@ -123,6 +123,8 @@ struct MergeResult {
 class Engine {
 public:
     explicit Engine(int device = 0) { check(qc_engine_create(device, &h_)); }
+    // with another error mapping (qcut_gpu::reference::check: the reference's own types)
+    Engine(int device, void (*chk)(int)) { chk(qc_engine_create(device, &h_)); }
     ~Engine() { qc_engine_destroy(h_); }
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -286,3 +288,90 @@ inline MergeResult chained_merge(Engine& e, const CandidatePool& pool, const Gra
 }
 
 }  // namespace qcut_gpu
+
+// ---------------------------------------------------------------------------
+// The reference's own types. Define QCUT_GPU_REFERENCE_TYPES after including the
+// reference's <qcut/qaoa.hpp> (or <qcut/pipeline.hpp>): these overloads take qcut::Graph
+// and qcut::SolveOptions, return qcut::SolveResult, and rethrow the engine's codes as
+// qcut::config_error / resource_error / io_error, so the call site at pipeline.hpp:263 and
+// the stage guard at pipeline.hpp:137-159 stay as they are (tests/cpp/ref_pipeline.cpp runs
+// the reference's run_pipeline with only its QAOA stage replaced by reference::solve_batch).
+// ---------------------------------------------------------------------------
+#ifdef QCUT_GPU_REFERENCE_TYPES
+namespace qcut_gpu::reference {
+
+inline void check(int rc) {
+    if (rc == QC_OK) return;
+    const std::string msg = qc_last_error();
+    switch (rc) {
+        case QC_ERR_CONFIG: throw qcut::config_error(msg);
+        case QC_ERR_RESOURCE: throw qcut::resource_error(msg);
+        case QC_ERR_IO: throw qcut::io_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+inline Engine& default_engine(int device = 0) {  // one per process, created on first use
+    static Engine e(device, &check);
+    return e;
+}
+
+inline qc_graph view(const qcut::Graph& g) {  // graph.hpp:21-25 Edge {u, v, w} == qc_edge
+    static_assert(sizeof(qcut::Edge) == sizeof(qc_edge), "qcut::Edge layout must match qc_edge");
+    return qc_graph{static_cast<int32_t>(g.n()), static_cast<int32_t>(g.edge_count()),
+                    reinterpret_cast<const qc_edge*>(g.edges().data())};
+}
+
+// pipeline.hpp:239-263: the whole QAOA stage as one batched device call
+inline std::vector<qcut::SolveResult> solve_batch(Engine& e, const std::vector<const qcut::Graph*>& graphs,
+                                                  const std::vector<qcut::SolveOptions>& opts) {
+    const std::size_t n = graphs.size();
+    if (opts.size() != n) throw qcut::config_error("one SolveOptions per graph");
+    std::vector<qc_graph> gv(n);
+    std::vector<qc_solve_options> ov(n);
+    std::vector<qc_solve_result> rv(n);
+    std::vector<std::vector<std::uint32_t>> bits(n);
+    std::vector<std::vector<double>> probs(n), params(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        gv[i] = view(*graphs[i]);
+        const qcut::SolveOptions& o = opts[i];
+        qc_solve_options& c = ov[i];
+        c = qc_solve_options{};
+        c.top_k = o.top_k;
+        c.layers = o.layers;
+        c.budget = o.budget;
+        c.fold = o.fold ? 1 : 0;
+        c.seed = o.seed;
+        c.qubit_cap = o.qubit_cap;
+        c.tolerance = o.tolerance;
+        c.threads = o.threads;
+        bits[i].resize(static_cast<std::size_t>(o.top_k > 0 ? o.top_k : 1));
+        probs[i].resize(bits[i].size());
+        params[i].resize(2 * static_cast<std::size_t>(o.layers > 0 ? o.layers : 1));
+        rv[i] = qc_solve_result{0, 0, 0, 0, 0.0, bits[i].data(), probs[i].data(), params[i].data()};
+    }
+    check(qc_solve_batch(e.handle(), gv.data(), static_cast<int>(n), ov.data(), rv.data()));
+    std::vector<qcut::SolveResult> out(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        qcut::SolveResult& r = out[i];
+        r.candidates.width = rv[i].width;
+        r.candidates.folded = rv[i].folded != 0;
+        for (int k = 0; k < rv[i].count; ++k)
+            r.candidates.entries.push_back({bits[i][static_cast<std::size_t>(k)], probs[i][static_cast<std::size_t>(k)]});
+        const auto p = static_cast<long>(opts[i].layers);
+        r.params.gammas.assign(params[i].begin(), params[i].begin() + p);
+        r.params.betas.assign(params[i].begin() + p, params[i].begin() + 2 * p);
+        r.expectation = rv[i].expectation;
+        r.evals = rv[i].evals;
+    }
+    return out;
+}
+
+// qaoa.hpp:198 solve_subgraph, on the process's default engine: the one-line replacement
+// of the call at pipeline.hpp:263
+inline qcut::SolveResult solve_subgraph(const qcut::Graph& g, const qcut::SolveOptions& so = {}) {
+    return solve_batch(default_engine(), {&g}, {so})[0];
+}
+
+}  // namespace qcut_gpu::reference
+#endif

@@ -799,7 +799,12 @@ int qc_engine_create(int device, qc_engine** out) {
     return guarded([&] {
         if (!out) config_error("null output pointer");
         int count = 0;
-        QC_CUDA(cudaGetDeviceCount(&count));
+        // no driver / no device is a resource failure (errors.hpp:14), not an internal one
+        const cudaError_t dc = cudaGetDeviceCount(&count);
+        if (dc != cudaSuccess) {
+            cudaGetLastError();
+            resource_error(std::string("no CUDA device: ") + cudaGetErrorString(dc));
+        }
         if (device < 0 || device >= count)
             resource_error("CUDA device " + std::to_string(device) + " not available");
         QC_CUDA(cudaSetDevice(device));
