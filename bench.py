@@ -508,12 +508,15 @@ def main():
         def step_value():
             return sess.execute()
     else:
-        from paper_2603_26232_b200.distributed import solve_sharded
+        from paper_2603_26232_b200.distributed import ShardedSession
         M = eng.subgraph_count(w["n"], edges, **cfg)
+        # resident like N=1: partition + this rank's cut tables once (qc_pipeline_prepare with
+        # shard_count = world), then per step: this rank's block of the QAOA stage, one NCCL
+        # all-gather of the solve records, merge on rank 0 with the session's partition
+        shard = ShardedSession(eng, w["n"], edges, rank, world, device=coll_dev, **cfg)
 
         def step_value():
-            # shard the QAOA stage, one NCCL all-gather of solve records, merge on rank 0
-            return solve_sharded(eng, w["n"], edges, rank, world, device=coll_dev, **cfg)
+            return shard.step()
 
     def timed(fn, steps, prof=False):
         """per-step device time via CUDA events on the engine stream, L2 flushed between."""

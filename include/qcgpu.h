@@ -319,6 +319,19 @@ void qc_pipeline_destroy(qc_pipeline* pl);
 int qc_pipeline_records(const qc_pipeline* pl, void* records, int64_t capacity,
                         int64_t* record_bytes, int32_t* subgraphs);
 
+/* Sharded resident session (one process per GPU; replaces the rounds loop of
+ * pipeline.hpp:271-280 for this rank's share): qc_pipeline_prepare with cfg->shard_count > 1
+ * partitions once and builds device cut tables only for this rank's contiguous block
+ * (qc_shard_range(M, shard_index, shard_count)); qc_pipeline_execute_shard runs that
+ * block's QAOA stage and writes its (end - begin) solve records (record size from
+ * qc_pipeline_records(pl, NULL, ...)); after the gather (qc_gather_topk), the rank holding
+ * all M records merges them with qc_pipeline_merge_records (pipeline.hpp:298-334) without
+ * partitioning again. */
+int qc_pipeline_execute_shard(qc_pipeline* pl, void* records, int64_t capacity, int32_t* begin,
+                              int32_t* end, double* qaoa_s);
+int qc_pipeline_merge_records(qc_pipeline* pl, const void* records, int64_t capacity,
+                              qc_run_report* report, char* assignment);
+
 /* ---- multi-GPU: shards of subgraphs, one gather of solve records ----
  * Solve record (fixed size per run, qc_run_record_bytes): int32 {width, count, evals,
  * folded}, double expectation, uint32 bits[kcap] (padded to 8 bytes), double probs[kcap],

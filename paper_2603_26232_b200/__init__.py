@@ -788,6 +788,41 @@ class PipelineSession:
                          rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
                          asg.value.decode())
 
+    def geometry(self) -> tuple[int, int]:
+        """(record bytes, M) of the session's run (qc_pipeline_records without a buffer)."""
+        rb = C.c_int64(0)
+        M = C.c_int32(0)
+        _check(self.engine.lib, self.engine.lib.qc_pipeline_records(self._h, None, C.c_int64(0),
+                                                                    C.byref(rb), C.byref(M)))
+        return int(rb.value), int(M.value)
+
+    def execute_shard(self) -> np.ndarray:
+        """Sharded session (shard_count > 1): this rank's block of the QAOA stage
+        (qc_pipeline_execute_shard) -> its packed solve records (uint8)."""
+        lib = self.engine.lib
+        rb, _ = self.geometry()
+        b = C.c_int32(0)
+        e = C.c_int32(0)
+        _check(lib, lib.qc_pipeline_execute_shard(self._h, None, C.c_int64(0), C.byref(b), C.byref(e),
+                                                  None))
+        n = e.value - b.value
+        buf = np.zeros(max(n * rb, 1), np.uint8)
+        q = C.c_double(0)
+        _check(lib, lib.qc_pipeline_execute_shard(self._h, _p(buf), C.c_int64(buf.size), C.byref(b),
+                                                  C.byref(e), C.byref(q)))
+        return buf[: n * rb]
+
+    def merge_records(self, records: np.ndarray) -> RunReport:
+        """pipeline.hpp:298-334 on all M gathered records (qc_pipeline_merge_records)."""
+        rec = np.ascontiguousarray(records, np.uint8)
+        rep = _RunReport()
+        asg = C.create_string_buffer(self.n + 1)
+        _check(self.engine.lib, self.engine.lib.qc_pipeline_merge_records(
+            self._h, _p(rec), C.c_int64(rec.size), C.byref(rep), asg))
+        return RunReport(rep.cut, rep.candidates_evaluated, rep.partition_s, rep.qaoa_s,
+                         rep.merge_s, rep.total_s, rep.subgraphs, bool(rep.windowed), rep.evals,
+                         asg.value.decode())
+
     def records(self) -> list:
         """SolveResults of the last execute() (qc_pipeline_records), in subgraph order."""
         lib = self.engine.lib

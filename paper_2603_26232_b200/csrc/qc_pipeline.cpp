@@ -532,10 +532,16 @@ struct qc_pipeline {
     HostGraph g;
     Partition P;
     std::vector<qc_solve_options> opts;
-    qcg::DevBuf tables;  // resident device cut tables of every subgraph
+    qcg::DevBuf tables;  // resident device cut tables of every subgraph (of this shard)
     std::vector<DevGraph> dg;
     double partition_s = 0.0;
     std::vector<SolveOut> last;  // SolveResults of the last execute (qc_pipeline_records)
+    // sharded session (cfg.shard_count > 1): this rank's contiguous block [begin, end)
+    int begin = 0, end = 0;
+    std::vector<HostGraph> shard_local;
+    std::vector<qc_solve_options> shard_opts;
+    int kcap = 1;
+    int64_t rb = 0;  // record bytes of the run (widest piece of the whole partition)
 };
 
 extern "C" {
@@ -546,7 +552,6 @@ int qc_pipeline_prepare(qc_engine* e, const qc_graph* g, const qc_run_config* cf
         if (!e || !out) config_error("null argument");
         QC_CUDA(cudaSetDevice(e->device));
         check_config(cfg);
-        if (cfg->shard_count != 1) config_error("qc_pipeline_* is single-shard");
         auto pl = std::make_unique<qc_pipeline>();
         pl->e = e;
         pl->cfg = *cfg;
@@ -570,14 +575,87 @@ int qc_pipeline_prepare(qc_engine* e, const qc_graph* g, const qc_run_config* cf
             pl->opts.push_back(so);
         }
         validate_solve(pl->P.local, pl->opts);
-        pl->dg = e->prepare(pl->P.local, true, false, &pl->tables);
+        int maxw = 1;
+        for (const auto& L : pl->P.local) maxw = std::max(maxw, L.n);
+        pl->kcap = kcap_of(cfg, maxw);
+        pl->rb = record_bytes(pl->kcap, cfg->layers);
+        if (cfg->shard_count > 1) {  // only this rank's block gets device tables
+            int32_t b = 0, en = 0;
+            if (qc_shard_range(M, cfg->shard_index, cfg->shard_count, &b, &en) != 0)
+                config_error("invalid shard request");
+            pl->begin = b;
+            pl->end = en;
+            pl->shard_local.assign(pl->P.local.begin() + b, pl->P.local.begin() + en);
+            pl->shard_opts.assign(pl->opts.begin() + b, pl->opts.begin() + en);
+            pl->dg = e->prepare(pl->shard_local, true, false, &pl->tables);
+        } else {
+            pl->begin = 0;
+            pl->end = M;
+            pl->dg = e->prepare(pl->P.local, true, false, &pl->tables);
+        }
         *out = pl.release();
+    });
+}
+
+int qc_pipeline_execute_shard(qc_pipeline* pl, void* records, int64_t capacity, int32_t* begin,
+                              int32_t* end, double* qaoa_s) {
+    return guarded([&] {
+        if (!pl) config_error("null pipeline");
+        if (pl->cfg.shard_count <= 1) config_error("qc_pipeline_execute_shard needs a sharded session");
+        qc_engine* e = pl->e;
+        QC_CUDA(cudaSetDevice(e->device));
+        const int n = pl->end - pl->begin;
+        if (begin) *begin = pl->begin;
+        if (end) *end = pl->end;
+        if (!records) return;
+        if (capacity < pl->rb * n)
+            config_error("record buffer holds " + std::to_string(capacity) + " bytes, the shard needs " +
+                         std::to_string(pl->rb * n) + " (qc_pipeline_records)");
+        const auto t0 = std::chrono::steady_clock::now();
+        pl->last = n ? solve_prepared(e, pl->shard_local, pl->dg, pl->shard_opts) : std::vector<SolveOut>{};
+        for (int k = 0; k < n; ++k)
+            pack_record(pl->last[static_cast<size_t>(k)], pl->kcap, pl->cfg.layers,
+                        static_cast<char*>(records) + static_cast<int64_t>(k) * pl->rb);
+        if (qaoa_s) *qaoa_s = seconds_since(t0);
+    });
+}
+
+int qc_pipeline_merge_records(qc_pipeline* pl, const void* records, int64_t capacity, qc_run_report* report,
+                              char* assignment) {
+    return guarded([&] {
+        if (!pl) config_error("null pipeline");
+        qc_engine* e = pl->e;
+        QC_CUDA(cudaSetDevice(e->device));
+        const int M = static_cast<int>(pl->P.first.size());
+        if (capacity < pl->rb * M)
+            config_error("record buffer holds " + std::to_string(capacity) + " bytes, " + std::to_string(M) +
+                         " records need " + std::to_string(pl->rb * M));
+        std::vector<SolveOut> solves;
+        solves.reserve(static_cast<size_t>(M));
+        for (int i = 0; i < M; ++i)
+            solves.push_back(unpack_record(static_cast<const char*>(records) + static_cast<int64_t>(i) * pl->rb,
+                                           pl->kcap, pl->cfg.layers));
+        const auto t0 = std::chrono::steady_clock::now();
+        bool windowed = false;
+        const MergeOutput out = merge_stage(e, pl->g, pl->P, solves, &pl->cfg, &windowed);
+        qc_run_report r{};
+        r.merge_s = seconds_since(t0);
+        r.partition_s = pl->partition_s;
+        r.subgraphs = M;
+        r.cut = out.value;
+        r.candidates_evaluated = out.leaves;
+        r.windowed = windowed ? 1 : 0;
+        for (const auto& sv : solves) r.evals += static_cast<uint64_t>(sv.evals);
+        if (report) *report = r;
+        write_assignment(out.assignment, assignment);
     });
 }
 
 int qc_pipeline_execute(qc_pipeline* pl, qc_run_report* report, char* assignment) {
     return guarded([&] {
         if (!pl) config_error("null pipeline");
+        if (pl->cfg.shard_count > 1)
+            config_error("sharded session: qc_pipeline_execute_shard + qc_pipeline_merge_records");
         qc_engine* e = pl->e;
         QC_CUDA(cudaSetDevice(e->device));
         qc_run_report r{};
@@ -636,6 +714,7 @@ int qc_pipeline_records(const qc_pipeline* pl, void* records, int64_t capacity, 
         if (bytes) *bytes = rb;
         if (subgraphs) *subgraphs = M;
         if (!records) return;
+        if (pl->cfg.shard_count > 1) config_error("sharded session: records come from qc_pipeline_execute_shard");
         if (pl->last.size() != static_cast<size_t>(M)) config_error("pipeline has not been executed");
         if (capacity < rb * M) config_error("record buffer too small");
         for (int i = 0; i < M; ++i)

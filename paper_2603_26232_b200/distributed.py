@@ -56,3 +56,27 @@ def solve_sharded(engine, n: int, edges, rank: int, world: int, device=None, **c
     if rank == 0:
         return engine.merge_records(n, edges, allrec, M, **cfg)
     return None
+
+
+class ShardedSession:
+    """Resident sharded solve (one process per GPU): the partition and this rank's device
+    cut tables are built once (qc_pipeline_prepare with shard_count = world); each step()
+    runs this rank's block of the QAOA stage, all-gathers the fixed-size records once and
+    merges on rank 0 with the session's partition (qc_pipeline_merge_records) — no
+    re-partition of the edge list per step. Returns the RunReport on rank 0, None elsewhere."""
+
+    def __init__(self, engine, n: int, edges, rank: int, world: int, device=None, **cfg):
+        self.rank, self.world, self.device = rank, world, device
+        self.sess = engine.prepare_pipeline(n, edges, shard_index=rank, shard_count=world, **cfg)
+        self.rb, self.M = self.sess.geometry()
+        self.bounds = shard_bounds(engine, self.M, world)
+
+    def step(self):
+        rec = self.sess.execute_shard()
+        allrec = gather_records(rec, self.bounds, self.rb, self.rank, device=self.device)
+        if self.rank == 0:
+            return self.sess.merge_records(allrec)
+        return None
+
+    def close(self):
+        self.sess.close()

@@ -87,20 +87,42 @@ def test_sharded_narrow_pieces_all_classes(engine):
         other.close()
 
 
+@pytest.mark.parametrize("mode", ["oneshot", "session"])
 @pytest.mark.parametrize("n,p,cfg", [
     (400, 0.1, dict(qubit_cap=20, top_k=2, layers=2, budget=8, seed=0)),   # config-2 shape
     (100, 0.1, C1),                                                          # config 1
 ])
-def test_torchrun_two_ranks_gloo(engine, tmp_path, n, p, cfg):
+def test_torchrun_two_ranks_gloo(engine, tmp_path, n, p, cfg, mode):
     from paper_2603_26232_b200 import generate_er
     out = tmp_path / "rank0.json"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000),
            os.path.join(ROOT, "tests", "gpu_sharded_run.py"), str(out), str(n), str(p),
-           json.dumps(cfg)]
+           json.dumps(cfg), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     got = json.loads(out.read_text())
     single = engine.run_pipeline(n, generate_er(n, p, 0), **cfg)
     assert got["cut"] == single.cut and got["assignment"] == single.assignment
     assert got["leaves"] == single.candidates_evaluated and got["evals"] == single.evals
+
+
+def test_sharded_session_single_process(engine):
+    """qc_pipeline_prepare with shard_count = 3 on one engine per shard: each session holds
+    only its block's cut tables; concatenated records merged by one session equal the
+    single-GPU pipeline (cut, assignment, leaves, evals), twice in a row."""
+    from paper_2603_26232_b200 import generate_er
+    e = generate_er(400, 0.1, 0)
+    cfg = dict(qubit_cap=20, top_k=2, layers=2, budget=8, seed=0)
+    single = engine.run_pipeline(400, e, **cfg)
+    sessions = [engine.prepare_pipeline(400, e, shard_index=r, shard_count=3, **cfg) for r in range(3)]
+    try:
+        rb, M = sessions[0].geometry()
+        assert M == 21
+        for _ in range(2):
+            recs = np.concatenate([s.execute_shard() for s in sessions])
+            assert recs.size == rb * M
+            _same(sessions[1].merge_records(recs), single)
+    finally:
+        for s in sessions:
+            s.close()
