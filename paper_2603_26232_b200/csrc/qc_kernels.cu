@@ -989,7 +989,15 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         // (profiles/r1_blocksum_stages.txt).
         const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl, 8);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
-        if (warps <= sms)
+        // Ring depth: 3 stages (two warp-CTAs per SM) by default. With two chunk streams the
+        // two chunks' block sums often run at once (C2: 80 + 88 warps > 148 SMs), and 6-stage
+        // warp-CTAs (one per SM) then serialise on 20 SMs: C2 69.6 -> 69.0 ms per solve with
+        // 3. QCG_SUM_STAGES=6 restores the deeper ring whenever every warp has an SM.
+        static const int sum_stages = [] {
+            const char* e = std::getenv("QCG_SUM_STAGES");
+            return e ? std::atoi(e) : 3;
+        }();
+        if (sum_stages == 6 && warps <= sms)
             launch_ex(k_blocksum<6, 8>, dim3(warps), dim3(32), sum_smem<6, 8>(), stream, pdl_ok, tmap, n_slots,
                       Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
         else

@@ -29,7 +29,11 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=(64, 32))
     ap.add_argument("--per-launch", action="store_true",
                     help="also report pass_low us per rep (spread of a sporadic slow run)")
+    ap.add_argument("--lib", default="", help="load this libqcgpu build instead (A/B runs)")
     a = ap.parse_args()
+    if a.lib:
+        import paper_2603_26232_b200 as pkg
+        pkg._LIB = pkg.load_library(a.lib)
     eng = Engine(0)
     if a.precision == 32:
         eng.set_precision(32)
