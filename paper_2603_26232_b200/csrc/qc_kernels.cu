@@ -628,7 +628,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // 32 lanes (one block each) read one part conflict-free.
 template <int kSumStages, int kSumParts>
 __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
-                                                int n_slots, int Q, int sym,
+                                                int n_slots, int Q, int sym, int pair_dirs,
                                                 double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
@@ -651,8 +651,12 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     const int slot = blockIdx.x / wps;
     if (slot >= n_slots) return;
     const int wis = blockIdx.x - slot * wps;
-    const bool desc = wis >= wpd;
-    const int b0 = (desc ? wis - wpd : wis) * bpw;   // first block (within the slot)
+    // SYM: the ascending and the descending warp of a block group are adjacent CTAs, so
+    // they run together and the second read of each stored block can hit L2 (at 24+ qubits
+    // f does not fit in L2 and the sum is bound by its read stream)
+    const bool desc = sym && pair_dirs ? (wis & 1) : wis >= wpd;
+    const int grp = sym && pair_dirs ? (wis >> 1) : (desc ? wis - wpd : wis);
+    const int b0 = grp * bpw;                         // first block (within the slot)
     const int gb0 = slot * nbl + b0;                 // first block (tensor coordinate)
     constexpr int kChunks = kBlock / kSumChunk;
     if (lane < kSumStages)
@@ -993,16 +997,20 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         // two chunks' block sums often run at once (C2: 80 + 88 warps > 148 SMs), and 6-stage
         // warp-CTAs (one per SM) then serialise on 20 SMs: C2 69.6 -> 69.0 ms per solve with
         // 3. QCG_SUM_STAGES=6 restores the deeper ring whenever every warp has an SM.
+        static const int pair_dirs = [] {  // QCG_SUM_PAIR=0: ascending warps, then descending
+            const char* e = std::getenv("QCG_SUM_PAIR");
+            return e ? std::atoi(e) : 1;
+        }();
         static const int sum_stages = [] {
             const char* e = std::getenv("QCG_SUM_STAGES");
             return e ? std::atoi(e) : 3;
         }();
         if (sum_stages == 6 && warps <= sms)
             launch_ex(k_blocksum<6, 8>, dim3(warps), dim3(32), sum_smem<6, 8>(), stream, pdl_ok, tmap, n_slots,
-                      Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+                      Q, plan.sym ? 1 : 0, pair_dirs, d_partials, d_tickets, d_out);
         else
             launch_ex(k_blocksum<3, 8>, dim3(warps), dim3(32), sum_smem<3, 8>(), stream, pdl_ok, tmap, n_slots,
-                      Q, plan.sym ? 1 : 0, d_partials, d_tickets, d_out);
+                      Q, plan.sym ? 1 : 0, pair_dirs, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());
