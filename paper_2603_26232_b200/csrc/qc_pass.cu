@@ -1584,10 +1584,12 @@ bool b5_plan(const HighPass& hp, int Q, bool fp32, B5Plan& P) {
     P.strides[3] = ab << hi;
     return (nt + P.hm + npad) == kHighBits && b5_lookup(nt, P.hm, fp32) != nullptr;
 }
-// Pass B kernel: the TMA kernel (tensor stores) where it measured faster: fp64 at Q >= 21
-// (at Q <= 19 v4's per-thread gathers are as fast or faster), fp32 at every size (v4 moves
-// fp32 in 8-byte cp.async / STG per amplitude: q=20 65 -> 54 us, q=26 372 -> 255 us)
-// (profiles/r1_pass_b_tma.txt). QCG_PASS_B=v4|tma forces one.
+// Pass B kernel: the TMA kernel (tensor stores) where it measured faster: fp64 at Q >= 25
+// (q=26: 8 slots 1687 -> 1505 us with its early stage refill; at q = 20..25 v4's
+// per-thread gathers are 3-7% faster in round 2: q=24 x 12 slots 544 vs 527 us, C3
+// 1311 -> 1275 ms per solve), fp32 at every size (v4 moves fp32 in 8-byte cp.async / STG
+// per amplitude: q=20 65 -> 54 us, q=26 372 -> 255 us) (profiles/r1_pass_b_tma.txt).
+// QCG_PASS_B=v4|tma forces one.
 bool tma_pass_b(int Q, bool fp32) {
     static const int mode = [] {
         const char* e = std::getenv("QCG_PASS_B");
@@ -1595,7 +1597,7 @@ bool tma_pass_b(int Q, bool fp32) {
         if (e && std::string(e) == "tma") return 1;
         return 2;
     }();
-    return mode == 1 || (mode == 2 && (fp32 || Q >= 21));
+    return mode == 1 || (mode == 2 && (fp32 || Q >= 25));
 }
 }  // namespace
 
