@@ -111,6 +111,7 @@ enum : uint32_t {
     F_TSTORE = 128u,    // pass B (TMA): results leave by tensor stores (default)
     F_B5EARLY = 512u,   // pass B (TMA): refill a stored stage before the next tile's wait
     F_NOLEVREG = 256u,  // pass B (v4) f pass: levels read after the refill (experiment)
+    F_A7EARLY = 2048u,  // split-buffer pass A: release the output buffer right after its store
     F_WHT = 1024u,      // fp32 mode only: Walsh–Hadamard form of the RX mixer (qc_amp.cuh)
 };
 
