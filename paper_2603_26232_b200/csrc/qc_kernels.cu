@@ -16,10 +16,10 @@
 // phase LUT is the host's std::polar table, and the expectation reproduces
 // blocked_sum's association: sequential within 4096-blocks, partials in block order.
 //
-// Passes (Q > 12), one HBM round trip each:
-//   pass A  (k_pass_low):  2^12 contiguous amps per CTA, [init |+>] + phase + RX 0..11
-//   pass Bk (k_pass_high): 9 gather bits x 8-amp columns per CTA, RX on bits >= 12,
-//                          mirror op last; the final one emits f(z)=|a|^2 C(z)
+// Passes (Q > 12), one HBM round trip each (qc_pass.cu):
+//   pass A:  2^12 contiguous amps per tile, [init |+>] + phase + RX 0..11
+//   pass B:  9 gather bits x 8-amp columns per tile, RX on bits >= 12, mirror op last;
+//            the final one emits f(z)=|a|^2 C(z)
 //   k_blocksum: the blocked sequential expectation over f (+ the in-order block sum).
 // Q <= 12 (k_onchip): the whole state lives in one CTA's shared memory for all layers.
 #include <cuda.h>
@@ -381,223 +381,6 @@ __global__ void __launch_bounds__(kFsumThreads) k_fsum_f32(const float* __restri
     }
 }
 
-// ---------------------------------------------------------------------------
-// Pass kernels: 512 threads x 8 amplitudes per 4096-amp tile, rounds of 3 targets in
-// registers exchanged through shared memory. 8 amps/thread keeps registers <= 64 so
-// two CTAs (32 warps) share an SM and one CTA's global loads overlap the other's FP64
-// rounds. Shared layout: e ^ ((e >> 3) & 7) (the 128-byte XOR swizzle) is
-// conflict-free for every round's 16-byte accesses.
-// ---------------------------------------------------------------------------
-constexpr int kPassThreads = 512;
-constexpr int kLutSmem = 512;  // LUT entries staged in shared memory (else read from L1/L2)
-constexpr size_t kPassSmem = 4096 * sizeof(double2) + kLutSmem * sizeof(double2);
-
-__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 3) & 7u); }
-
-// RX on the 3 thread-local bits (ascending) of a[8].
-__device__ __forceinline__ void rx_local3(double2 (&a)[8], double c, double s) {
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (!(j & (1 << b))) rx_rn(a[j], a[j | (1 << b)], c, s);
-    }
-}
-
-// k_pass_low: pass A, tile = 4096 contiguous stored amplitudes, targets 0..11
-// (rounds: bits 0-2, 3-5, 6-8, 9-11), [|+> init] + phase first.
-__global__ void __launch_bounds__(kPassThreads, 2) k_pass_low(const SlotDesc* __restrict__ slots,
-                                                            const LayerParam* __restrict__ lp,
-                                                            int layer, int Q, uint32_t flags) {
-    extern __shared__ __align__(16) double2 sm[];
-    double2* slut = sm + 4096;
-    const int tshift = Q - 12;
-    const int slot = blockIdx.x >> tshift;
-    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
-    const SlotDesc S = slots[slot];
-    const LayerParam L = lp[S.layer_base + layer];
-    const bool init = flags & F_INIT;
-    if (!init && !L.phase && !L.mix) return;  // identity layer: memory already holds it
-    const uint32_t base = tile << 12;
-    double2* __restrict__ st = S.state + base;
-    const uint32_t tid = threadIdx.x;
-    double2 a[8];
-    // issue every global load up front: amplitudes (coalesced), levels (one 16-byte
-    // vector per thread, the 8 levels of its round-0 amplitudes), LUT -> shared
-    if (!init) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) a[k] = st[k * kPassThreads + tid];
-    }
-    const bool use_lev = L.phase && S.plev;
-    uint4 lv4 = make_uint4(0, 0, 0, 0);
-    if (use_lev) lv4 = *reinterpret_cast<const uint4*>(S.plev + base + tid * 8u);
-    const bool lut_sm = use_lev && L.lut_len <= kLutSmem;
-    if (lut_sm)
-        for (int i = tid; i < L.lut_len; i += kPassThreads) slut[i] = L.lut[i];
-    if (!init) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) sm[swz(k * kPassThreads + tid)] = a[k];
-    }
-    __syncthreads();
-    // round 0: bits 0..2 (e = tid*8 + j), phase first
-    {
-        const uint32_t lvw[4] = {lv4.x, lv4.y, lv4.z, lv4.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t e = tid * 8u + j;
-            double2 v = init ? make_double2(S.amp0, 0.0) : sm[swz(e)];
-            if (L.phase) {
-                if (use_lev) {
-                    const uint32_t lev = (lvw[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-                    v = cmul_rn(v, lut_sm ? slut[lev] : L.lut[lev]);
-                } else {
-                    v = phase_rn(v, S, L, base + e);
-                }
-            }
-            a[j] = v;
-        }
-        if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sm[swz(tid * 8u + j)] = a[j];
-    }
-    __syncthreads();
-    // round 1: bits 3..5 (e = (tid>>3)<<6 | j<<3 | tid&7)
-    {
-        const uint32_t r = ((tid >> 3) << 6) | (tid & 7u);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 3))];
-        if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sm[swz(r | (j << 3))] = a[j];
-    }
-    __syncthreads();
-    // round 2: bits 6..8 (e = (tid>>6)<<9 | j<<6 | tid&63)
-    {
-        const uint32_t r = ((tid >> 6) << 9) | (tid & 63u);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = sm[swz(r | (j << 6))];
-        if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sm[swz(r | (j << 6))] = a[j];
-    }
-    __syncthreads();
-    // round 3: bits 9..11 (e = j<<9 | tid), stored straight back (coalesced)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) a[j] = sm[swz((j << 9) | tid)];
-    if (L.mix) rx_local3(a, L.c, L.s);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) st[(j << 9) | tid] = a[j];
-}
-
-// ---------------------------------------------------------------------------
-// k_pass_high: 3 column bits (8 contiguous amps, bits 0..2) x 9 tile bits per tile.
-// Tile bit kinds: 1 RX target (mask = one stored bit), 2 mirror (mask = all Q bits,
-// RX on qubit q-1), 0 batch (no op). Targets precede the mirror in tile-bit order.
-// In the mirror half of a tile (mirror bit set) every stored bit is complemented, so
-// the RX roles (a0 = bit clear) of target pairs swap. Rounds: tile bits 0-2, 3-5, 6-8;
-// shared index e = w | tilebits << 3 (lanes vary w: conflict-free without swizzle).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t tile_xor(const HighPass& hp, uint32_t bits) {
-    uint32_t x = 0;
-#pragma unroll
-    for (int b = 0; b < kHighBits; ++b)
-        if ((bits >> b) & 1u) x ^= hp.mask[b];
-    return x;
-}
-
-template <int OFF>
-__device__ __forceinline__ void high_round(double2 (&a)[8], const HighPass& hp, bool mir_thread,
-                                           double c, double s) {
-    constexpr int kNoLocal = -1;
-    const int mir_local = (hp.mpos >= OFF && hp.mpos < OFF + 3) ? hp.mpos - OFF : kNoLocal;
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-        const int kind = hp.kind[OFF + b];
-        if (kind == 0) continue;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            if (j & (1 << b)) continue;
-            if (kind == 2) {
-                rx_rn(a[j], a[j | (1 << b)], c, s);  // mirror: role order is immaterial
-            } else {
-                const bool mir = mir_thread ^ (mir_local >= 0 && ((j >> mir_local) & 1));
-                if (mir)
-                    rx_rn(a[j | (1 << b)], a[j], c, s);
-                else
-                    rx_rn(a[j], a[j | (1 << b)], c, s);
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kPassThreads, 2) k_pass_high(const SlotDesc* __restrict__ slots,
-                                                             const LayerParam* __restrict__ lp,
-                                                             int layer, int Q, HighPass hp,
-                                                             uint32_t flags) {
-    extern __shared__ __align__(16) double2 sm[];
-    const int tshift = Q - 12;
-    const int slot = blockIdx.x >> tshift;
-    const uint32_t tile = blockIdx.x & ((1u << tshift) - 1u);
-    const SlotDesc S = slots[slot];
-    const LayerParam L = lp[S.layer_base + layer];
-    const bool fout = flags & F_EXPECT;
-    const bool sout = !fout || (flags & F_STATE_OUT);
-    if (!L.mix && !fout) return;
-    const bool mix = L.mix;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t w = tid & 7u;
-    const uint32_t tb = tid >> 3;  // 6 tile bits held by the thread
-    const uint32_t x = deposit(tile, hp.freemask) | w;
-    const int mp = hp.mpos;
-    auto mbit = [&](uint32_t tilebits) { return mp >= 0 && ((tilebits >> mp) & 1u); };
-    double2 a[8];
-    // output addresses of round 2 (tile bits 0-5 = tb, 6-8 = j) and their levels, early
-    const uint32_t g2 = x ^ tile_xor(hp, tb);
-    uint32_t lv[8];
-    if (fout) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
-            lv[j] = S.lev ? S.lev[g] : 0u;
-        }
-    }
-    // round 0: tile bits 0-2 local, thread holds tile bits 3-8 = tb (coalesced by w)
-    {
-        const uint32_t tbits = tb << 3;
-        const uint32_t g0 = x ^ tile_xor(hp, tbits);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = S.state[g0 ^ tile_xor(hp, static_cast<uint32_t>(j))];
-        if (mix) high_round<0>(a, hp, mbit(tbits), L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sm[w | (j << 3) | (tb << 6)] = a[j];
-    }
-    __syncthreads();
-    // round 1: tile bits 3-5 local, thread holds tile bits 0-2 and 6-8
-    {
-        const uint32_t tbits = (tb & 7u) | ((tb >> 3) << 6);
-        const uint32_t e0 = w | ((tb & 7u) << 3) | ((tb >> 3) << 9);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = sm[e0 | (j << 6)];
-        if (mix) high_round<3>(a, hp, mbit(tbits), L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sm[e0 | (j << 6)] = a[j];
-    }
-    __syncthreads();
-    // round 2: tile bits 6-8 local, thread holds tile bits 0-5 = tb
-    {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) a[j] = sm[w | (tb << 3) | (j << 9)];
-        if (mix) high_round<6>(a, hp, mbit(tb), L.c, L.s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t g = g2 ^ tile_xor(hp, static_cast<uint32_t>(j) << 6);
-            if (sout) S.state[g] = a[j];
-            if (fout)
-                S.fbuf[g] = __dmul_rn(norm_rn(a[j]),
-                                      S.lev ? static_cast<double>(lv[j]) : (S.val ? S.val[g] : 1.0));
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // blocked expectation over f (statevector.hpp:48-65). Every 4096-block partial is a
@@ -899,21 +682,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         if (passes_done) QC_CUDA(cudaEventRecord(passes_done, stream));
         return 1;
     }
-    // (A persistent one-CTA-per-SM variant with a two-stage cp.async ring measured slower
-    // on B200: pass A 141 us / pass B 125 us vs 103 / 95 us for these 2-CTA/SM kernels.)
-    static PerDeviceOnce attrs;
-    attrs.run([] {
-        QC_CUDA(cudaFuncSetAttribute(k_pass_low, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kPassSmem)));
-        QC_CUDA(cudaFuncSetAttribute(k_pass_high, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(4096 * sizeof(double2))));
-    });
     int launches = 0;
-    const unsigned grid = static_cast<unsigned>(n_slots) << (Q - 12);
-    static const bool v3 = [] {
-        const char* e = std::getenv("QCG_PASS");
-        return e && std::atoi(e) == 3;
-    }();
     // Programmatic dependent launch for every kernel whose stream predecessor is a kernel
     // of this chain (the first one follows the staging copy). Off by default: with two
     // chunk streams the early-scheduled dependent CTAs hold SMs the other stream's kernels
@@ -931,11 +700,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         // FP64: 6 per amplitude for the phase, 6 per amplitude per RX target (12 targets)
         const double oa = (nph * 6.0 + nmix * 72.0) * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream, oa);
-        if (v3)
-            k_pass_low<<<grid, kPassThreads, kPassSmem, stream>>>(d_slots, d_lp, l, Q, fa);
-        else
-            launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok && l > 0,
-                           state_base);
+        launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok && l > 0,
+                       state_base);
         if (prof) prof->end(stream);
         ++launches;
         for (size_t h = 0; h < plan.high.size(); ++h) {
@@ -953,12 +719,8 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             // 6 per amplitude per pair op (RX target or mirror), + |a|^2 C(z) (4) when f is emitted
             const double oh = nmix * 6.0 * items * N + ((fh & F_EXPECT) ? n_slots * 4.0 * N : 0.0);
             if (prof) prof->begin(K_PASS_HIGH, bh, stream, oh);
-            if (v3)
-                k_pass_high<<<grid, kPassThreads, 4096 * sizeof(double2), stream>>>(
-                    d_slots, d_lp, l, Q, plan.high[h], fh);
-            else
-                launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok,
-                               state_base);
+            launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok,
+                           state_base);
             if (prof) prof->end(stream);
             ++launches;
         }
