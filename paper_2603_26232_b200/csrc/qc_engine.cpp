@@ -10,6 +10,7 @@
 #include <complex>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <map>
 #include <numbers>
 #include <unordered_set>
@@ -321,6 +322,14 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     stats.phase.assign(static_cast<size_t>(std::max(p, 0)), 0);
     stats.mix.assign(static_cast<size_t>(std::max(p, 0)), 0);
     const double amp0 = 1.0 / std::sqrt(static_cast<double>(size_t{1} << g0.q));  // :141
+    struct LutJob {
+        size_t pos;
+        int len;
+        double gamma;
+        const double* fv;
+    };
+    std::vector<LutJob> jobs;
+    jobs.reserve(static_cast<size_t>(n) * static_cast<size_t>(std::max(p, 1)));
     for (int k = 0; k < n; ++k) {
         const DevGraph& dgk = dg[static_cast<size_t>(pts[k].g)];
         SlotDesc& s = hs[k];
@@ -350,28 +359,46 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
             L.lut_len = 0;
             L.pad = 0;
             if (L.phase && dgk.lev && !dgk.unit_cost) {
-                // statevector.hpp:154-157: lut[c] = std::polar(1.0, -gamma * c); non-integral
-                // tables (:162-164): std::polar(1.0, -gamma * val) for each distinct val
-                const double* fv = dgk.fvals.empty() ? nullptr : dgk.fvals.data();
-                auto arg = [&](int c) { return -gamma * (fv ? fv[c] : static_cast<double>(c)); };
-                if (fp32) {
-                    float* dst = reinterpret_cast<float*>(h + o_lut) + 2 * lut_pos;
-                    for (int c = 0; c < dgk.lut_len; ++c) {
-                        const std::complex<double> z = std::polar(1.0, arg(c));
-                        dst[2 * c] = static_cast<float>(z.real());
-                        dst[2 * c + 1] = static_cast<float>(z.imag());
-                    }
-                } else {
-                    double* dst = hlut + 2 * lut_pos;
-                    for (int c = 0; c < dgk.lut_len; ++c) {
-                        const std::complex<double> z = std::polar(1.0, arg(c));
-                        dst[2 * c] = z.real();
-                        dst[2 * c + 1] = z.imag();
-                    }
-                }
+                jobs.push_back({lut_pos, dgk.lut_len, gamma, dgk.fvals.empty() ? nullptr : dgk.fvals.data()});
                 L.lut = reinterpret_cast<const double2*>(d + o_lut + lut_pos * lut_entry);
                 L.lut_len = dgk.lut_len;
                 lut_pos += static_cast<size_t>(dgk.lut_len);
+            }
+        }
+    }
+    // statevector.hpp:154-157 lut[c] = std::polar(1.0, -gamma * c); non-integral tables
+    // (:162-164) std::polar(1.0, -gamma * val) per distinct val. Host libm, exactly the
+    // reference's operation. The LUTs sit on the chunk step's host critical path (results
+    // in -> next step out), so from 256 entries they are split over 4 host threads (C2,
+    // ~400-800 entries per step: staging 2.6 -> 1.5 ms per solve, C2 69.0-69.3 -> 68.5-68.6
+    // ms). QCG_LUT_PAR_MIN / QCG_HOST_THREADS override.
+    static const size_t lut_par_min = [] {
+        const char* e = std::getenv("QCG_LUT_PAR_MIN");
+        return e ? static_cast<size_t>(std::atol(e)) : static_cast<size_t>(256);
+    }();
+    static const int lut_threads_env = [] {
+        const char* e = std::getenv("QCG_HOST_THREADS");
+        if (e) return std::max(1, std::atoi(e));
+        return static_cast<int>(std::max(1u, std::min(4u, std::thread::hardware_concurrency())));
+    }();
+    const int lut_threads = lut_pos >= lut_par_min ? lut_threads_env : 1;
+#pragma omp parallel for schedule(static) num_threads(lut_threads) if (lut_threads > 1)
+    for (size_t jb = 0; jb < jobs.size(); ++jb) {
+        const LutJob& J = jobs[jb];
+        auto arg = [&](int c) { return -J.gamma * (J.fv ? J.fv[c] : static_cast<double>(c)); };
+        if (fp32) {
+            float* dst = reinterpret_cast<float*>(h + o_lut) + 2 * J.pos;
+            for (int c = 0; c < J.len; ++c) {
+                const std::complex<double> z = std::polar(1.0, arg(c));
+                dst[2 * c] = static_cast<float>(z.real());
+                dst[2 * c + 1] = static_cast<float>(z.imag());
+            }
+        } else {
+            double* dst = hlut + 2 * J.pos;
+            for (int c = 0; c < J.len; ++c) {
+                const std::complex<double> z = std::polar(1.0, arg(c));
+                dst[2 * c] = z.real();
+                dst[2 * c + 1] = z.imag();
             }
         }
     }
