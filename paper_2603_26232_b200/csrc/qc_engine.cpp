@@ -265,6 +265,17 @@ void qc_engine::reserve(int Q, bool need_fbuf, size_t slots) {
     }
 }
 
+namespace {
+// results written by the kernels into pinned host memory (default) or copied (QCG_ZC=0)
+bool zero_copy_out() {
+    static const bool on = [] {
+        const char* e = std::getenv("QCG_ZC");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace
+
 void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
                               uint32_t flags, size_t slot0, ChunkCtx& ctx) {
     const auto t_enq = std::chrono::steady_clock::now();
@@ -407,11 +418,15 @@ void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* 
     if (ctx.wait_on) QC_CUDA(cudaStreamWaitEvent(cs, ctx.wait_on, 0));
     auto record = [&](size_t nbytes) {
         h2d_copy(d, h, nbytes, cs);
+        // the expectations go straight to the pinned host block (zero-copy: pinned memory is
+        // device-addressable under UVA), so no D2H copy node trails the block sum on the
+        // chunk step's critical path
         const int k = launch_chain(plan, reinterpret_cast<const SlotDesc*>(d),
                                    reinterpret_cast<const LayerParam*>(d + o_lp), n, p, flags,
-                                   reinterpret_cast<double*>(fb), part, tick, od, cs, &stats,
+                                   reinterpret_cast<double*>(fb), part, tick, (ho && zero_copy_out()) ? ho : od, cs, &stats,
                                    graph ? nullptr : &prof, st, ctx.passes);
-        if (ho) d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
+        if (ho && !zero_copy_out()) d2h_copy(ho, od, static_cast<size_t>(n) * 8, cs);
+        else if (ho) d2h += static_cast<uint64_t>(n) * 8;
         return k;
     };
     if (!graph) {
