@@ -737,27 +737,54 @@ std::vector<SolveOut> solve_prepared(qc_engine* e, const std::vector<HostGraph>&
             e->eval_chunk(dg, pts.data(), static_cast<int>(pts.size()), p,
                           F_INIT | F_STATE_OUT | e->fp_flag(),
                           nullptr);
+            // every state's top-K is queued at once (scratch per state; the small results land
+            // in pinned host memory, written by the kernels), spread over the engine's streams,
+            // then one wait: no per-subgraph copy + sync round trip
+            std::vector<size_t> soff(end - b + 1, 0), ooff(end - b + 1, 0);
+            for (size_t k = b; k < end; ++k) {
+                const size_t i = ids[k];
+                const int K = opts[i].top_k;
+                soff[k - b + 1] = soff[k - b] + ((topk_scratch_bytes(q, opts[i].fold != 0, K) + 255) & ~size_t{255});
+                ooff[k - b + 1] = ooff[k - b] + ((static_cast<size_t>(K) * 12 + 64 + 255) & ~size_t{255});
+            }
+            char* scratch0 = static_cast<char*>(e->topk_scratch.get(soff[end - b]));
+            char* host0 = static_cast<char*>(e->topk_host.get(ooff[end - b]));
+            const int nst = 4;
+            cudaEvent_t fork = nullptr;
+            QC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+            QC_CUDA(cudaEventRecord(fork, e->stream));  // the states are written on the main stream
+            for (int sidx = 1; sidx < nst; ++sidx) QC_CUDA(cudaStreamWaitEvent(e->aux[sidx - 1], fork, 0));
             for (size_t k = b; k < end; ++k) {
                 const size_t i = ids[k];
                 const int K = opts[i].top_k;
                 const bool fold = opts[i].fold != 0;
-                const size_t sb = topk_scratch_bytes(q, fold, K);
-                void* scratch = e->topk_scratch.get(sb);
-                char* ob = static_cast<char*>(e->topk_out.get(static_cast<size_t>(K) * 12 + 64));
+                char* ob = host0 + ooff[k - b];
                 auto* d_bits = reinterpret_cast<uint32_t*>(ob);
                 auto* d_probs = reinterpret_cast<double*>(ob + ((static_cast<size_t>(K) * 4 + 15) & ~size_t{15}));
+                const int sidx = static_cast<int>((k - b) % nst);
+                cudaStream_t sst = sidx == 0 ? e->stream : e->aux[sidx - 1];
                 e->launches += launch_topk(e->slot_state(q, dg[i].sym, static_cast<int>(k - b),
                                                          e->precision == 32),
-                                           q, dg[i].sym, fold, K, scratch, d_bits, d_probs, e->stream,
-                                           &e->prof, e->precision == 32);
+                                           q, dg[i].sym, fold, K, scratch0 + soff[k - b], d_bits, d_probs, sst,
+                                           sidx == 0 ? &e->prof : nullptr, e->precision == 32);
+                e->d2h += static_cast<uint64_t>(K) * 12;
+            }
+            for (int sidx = 1; sidx < nst; ++sidx) {  // join the side streams
+                QC_CUDA(cudaEventRecord(fork, e->aux[sidx - 1]));
+                QC_CUDA(cudaStreamWaitEvent(e->stream, fork, 0));
+            }
+            QC_CUDA(cudaEventDestroy(fork));
+            e->sync();
+            for (size_t k = b; k < end; ++k) {
+                const size_t i = ids[k];
+                const int K = opts[i].top_k;
+                const char* ob = host0 + ooff[k - b];
                 SolveOut& r = out[i];
                 r.width = q;
-                r.folded = fold;
-                r.bits.resize(static_cast<size_t>(K));
-                r.probs.resize(static_cast<size_t>(K));
-                e->d2h_copy(r.bits.data(), d_bits, static_cast<size_t>(K) * 4);
-                e->d2h_copy(r.probs.data(), d_probs, static_cast<size_t>(K) * 8);
-                e->sync();
+                r.folded = opts[i].fold != 0;
+                r.bits.assign(reinterpret_cast<const uint32_t*>(ob), reinterpret_cast<const uint32_t*>(ob) + K);
+                const auto* pr = reinterpret_cast<const double*>(ob + ((static_cast<size_t>(K) * 4 + 15) & ~size_t{15}));
+                r.probs.assign(pr, pr + K);
                 r.params = best[i].params;
                 r.expectation = best[i].expectation;
                 r.evals = best[i].evals;

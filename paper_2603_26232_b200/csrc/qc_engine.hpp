@@ -117,6 +117,7 @@ struct qc_engine {
     qcg::DevBuf tables, states, fbuf, partials, outd, stage, edges, topk_scratch, topk_out, tickets;
     qcg::DevBuf distinct;  // scratch of the non-integral tables' distinct-value search
     qcg::HostBuf hstage, hout;
+    qcg::HostBuf topk_host;  // final top-K results of a batch, written by the kernels (zero-copy)
     qcg::Prof prof;        // live per-kernel CUDA-event timing (qc_engine_profile)
     qcg::DeviceArena merge_arena;                           // merge scratch, reused
     std::vector<std::unique_ptr<qcg::ChunkCtx>> chunk_pool;  // per-chunk staging, reused
