@@ -271,32 +271,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         const S c = static_cast<S>(d.c), sn = static_cast<S>(d.s);
         const bool mix = d.mix;
         V a[16];
-        // round 0: bits 0-3, phase first
+        // round 0: bits 0-3, phase first. Two instantiations (staged LUT: LDS; global LUT:
+        // LDG) so the lookups do not compile to generic loads, as in k_pass_a5/a7.
         {
             const uint4* lv = reinterpret_cast<const uint4*>(sm + kOffLev + s * 8192u) + gt * 2u;
-            const V* lutp = lut_sm ? slut : reinterpret_cast<const V*>(d.lut);
             const bool phase = d.phase;
             const S amp0 = static_cast<S>(d.amp0);
+            auto round0 = [&](const V* __restrict__ lutp) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
+                for (int h = 0; h < 2; ++h) {
+                    const uint4 l4 = use_lev ? lv[h] : make_uint4(0, 0, 0, 0);
 #pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    const int j = h * 8 + jj;
-                    const uint32_t e = gt * 16u + j;
-                    V v = init ? Amp<V>::mk(amp0, S(0)) : st[sw<V>(e)];
-                    if (phase) {
-                        if (use_lev) {
-                            const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
-                                                : (jj >> 1) == 2 ? l4.z : l4.w;
-                            v = Amp<V>::cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
-                        } else {
-                            v = phase_frac<V>(v, d.gamma, d.val[base + e]);
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int j = h * 8 + jj;
+                        const uint32_t e = gt * 16u + j;
+                        V v = init ? Amp<V>::mk(amp0, S(0)) : st[sw<V>(e)];
+                        if (phase) {
+                            if (use_lev) {
+                                const uint32_t word = (jj >> 1) == 0 ? l4.x : (jj >> 1) == 1 ? l4.y
+                                                    : (jj >> 1) == 2 ? l4.z : l4.w;
+                                v = Amp<V>::cmul(v, lutp[(word >> ((jj & 1) * 16)) & 0xffffu]);
+                            } else {
+                                v = phase_frac<V>(v, d.gamma, d.val[base + e]);
+                            }
                         }
+                        a[j] = v;
                     }
-                    a[j] = v;
                 }
-            }
+            };
+            if (lut_sm)
+                round0(slut);
+            else
+                round0(reinterpret_cast<const V*>(d.lut));
             if (mix) mix4<V>(a, c, sn, wht);
 #pragma unroll
             for (int j = 0; j < 16; ++j) st[sw<V>(gt * 16u + j)] = a[j];
