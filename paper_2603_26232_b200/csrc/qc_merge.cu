@@ -298,9 +298,32 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(SearchArgs A, uint64_
 
 // Reduce block bests, decode the winning leaf, write its pieces into the device
 // assignment, advance the accumulated value and the leaf counter.
-__global__ void k_commit(SearchArgs A, int n_blocks, uint64_t* leaves_total, int* dead_end,
-                         double* acc, int64_t* iacc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+constexpr int kCommitThreads = 256;
+__global__ void __launch_bounds__(kCommitThreads) k_commit(SearchArgs A, int n_blocks, uint64_t* leaves_total,
+                                                           int* dead_end, double* acc, int64_t* iacc) {
+    // the window's winner over the search blocks' results: (value desc, leaf index asc),
+    // reduced by the whole CTA (a single thread walking ~10^3 block results in order
+    // waited on one global load at a time)
+    __shared__ int s_best[kCommitThreads];
+    const int t = threadIdx.x;
+    auto better = [&](int b, int c) {  // is block b's result better than block c's?
+        if (c < 0) return b >= 0;
+        if (b < 0) return false;
+        return A.integral ? (A.blk_ival[b] > A.blk_ival[c] ||
+                             (A.blk_ival[b] == A.blk_ival[c] && A.blk_idx[b] < A.blk_idx[c]))
+                          : (A.blk_val[b] > A.blk_val[c] ||
+                             (A.blk_val[b] == A.blk_val[c] && A.blk_idx[b] < A.blk_idx[c]));
+    };
+    int mine = -1;
+    for (int b = t; b < n_blocks; b += kCommitThreads)
+        if (A.blk_idx[b] != ~uint64_t{0} && better(b, mine)) mine = b;
+    s_best[t] = mine;
+    __syncthreads();
+    for (int off = kCommitThreads / 2; off > 0; off >>= 1) {
+        if (t < off && better(s_best[t + off], s_best[t])) s_best[t] = s_best[t + off];
+        __syncthreads();
+    }
+    if (t != 0 || blockIdx.x != 0) return;
     const int L = A.L;
     const int need0 = need_parity(A);
     uint64_t T = 0;
@@ -318,20 +341,7 @@ __global__ void k_commit(SearchArgs A, int n_blocks, uint64_t* leaves_total, int
         return;
     }
     *leaves_total += T;
-    int best = -1;
-    for (int b = 0; b < n_blocks; ++b) {
-        if (A.blk_idx[b] == ~uint64_t{0}) continue;
-        if (best < 0) {
-            best = b;
-            continue;
-        }
-        const bool take =
-            A.integral ? (A.blk_ival[b] > A.blk_ival[best] ||
-                          (A.blk_ival[b] == A.blk_ival[best] && A.blk_idx[b] < A.blk_idx[best]))
-                       : (A.blk_val[b] > A.blk_val[best] ||
-                          (A.blk_val[b] == A.blk_val[best] && A.blk_idx[b] < A.blk_idx[best]));
-        if (take) best = b;
-    }
+    const int best = s_best[0];
     if (best < 0) {
         *dead_end = 1;
         return;
@@ -937,7 +947,7 @@ MergeOutput run_merge(const MergeInput& in, const std::vector<Window>& windows, 
                 search(k_search<false, false>);
         }
         prof->begin(K_MERGE_OTHER, 0.0, st);
-        k_commit<<<1, 1, 0, st>>>(A, static_cast<int>(geo[w].blocks), d_leaves, d_dead, d_acc, d_iacc);
+        k_commit<<<1, kCommitThreads, 0, st>>>(A, static_cast<int>(geo[w].blocks), d_leaves, d_dead, d_acc, d_iacc);
         prof->end(st);
         *launches += integral ? 3 : 2;
         QC_CUDA(cudaGetLastError());
