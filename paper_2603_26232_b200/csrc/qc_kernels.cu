@@ -411,7 +411,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // 32 lanes (one block each) read one part conflict-free.
 template <int kSumStages, int kSumParts>
 __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
-                                                int n_slots, int Q, int sym, int pair_dirs,
+                                                int n_slots, int Q, int sym, int mode,
                                                 double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
                                                 double* __restrict__ out) {
@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     // SYM: the ascending and the descending warp of a block group are adjacent CTAs, so
     // they run together and the second read of each stored block can hit L2 (at 24+ qubits
     // f does not fit in L2 and the sum is bound by its read stream)
+    const bool pair_dirs = mode & 1;
     const bool desc = sym && pair_dirs ? (wis & 1) : wis >= wpd;
     const int grp = sym && pair_dirs ? (wis >> 1) : (desc ? wis - wpd : wis);
     const int b0 = grp * bpw;                         // first block (within the slot)
@@ -449,10 +450,35 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     asm volatile("griddepcontrol.wait;\n" ::: "memory");  // f is written by the previous pass
     // lane 0 issues, by predication rather than a branch, so the (uniform) issue code can
     // be scheduled into the gaps of the dependent add chain
+    // SYM with mode bit 1: L2 hints for the two reads of every stored part (the ascending
+    // chain of its block and the descending chain of the mirror block). Whichever warp of
+    // the pair reads a part first (c < kChunks/2) keeps it (evict_last) for the other; the
+    // second read (c >= kChunks/2) marks it evict_first.
+    const bool hint = sym && (mode & 2);
+    uint64_t pol_keep = 0, pol_drop = 0;
+    if (hint) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
+        if (mode & 4)
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol_drop));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_drop));
+    }
     auto issue = [&](int c) {
         if (c >= kChunks) return;
         const int st = c % kSumStages;
         const int part0 = (desc ? kChunks - 1 - c : c) * kSumParts;
+        if (hint) {
+            const uint64_t pol = 2 * c < kChunks ? pol_keep : pol_drop;
+            asm volatile(
+                "{\n .reg .pred p;\n setp.eq.u32 p, %6, 0;\n"
+                " @p mbarrier.arrive.expect_tx.shared.b64 _, [%5], %7;\n"
+                " @p cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+                "[%0], [%1, {%2, %3, %4}], [%5], %8;\n}\n" ::"r"(smem_u32(sbase + st * kSumStageBytes)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(gb0), "r"(part0), "r"(smem_u32(mbar + st)),
+                "r"(lane), "r"(static_cast<unsigned>(kSumStageBytes)), "l"(pol)
+                : "memory");
+            return;
+        }
         asm volatile(
             "{\n .reg .pred p;\n setp.eq.u32 p, %6, 0;\n"
             " @p mbarrier.arrive.expect_tx.shared.b64 _, [%5], %7;\n"
@@ -763,16 +789,25 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             const char* e = std::getenv("QCG_SUM_PAIR");
             return e ? std::atoi(e) : 1;
         }();
+        // L2 keep/drop hints on the two reads of each stored part (SYM): block sum at q = 22 /
+        // 24 / 26 118.6 -> 115.2, 176.8 -> 169.8, 261.4 -> 250.6 us per launch; at q = 20 (f
+        // fits L2) 38.5 -> 39.5, so on from Q = 21 stored bits. QCG_SUM_HINT=0/1 forces.
+        static const int sum_hint_env = [] {
+            const char* e = std::getenv("QCG_SUM_HINT");
+            return e ? std::atoi(e) : -1;
+        }();
+        const int sum_hint = sum_hint_env >= 0 ? sum_hint_env : (Q >= 21 ? 1 : 0);
+        const int sum_mode = (pair_dirs ? 1 : 0) | (sum_hint ? 2 : 0) | (sum_hint == 2 ? 4 : 0);
         static const int sum_stages = [] {
             const char* e = std::getenv("QCG_SUM_STAGES");
             return e ? std::atoi(e) : 3;
         }();
-        if (sum_stages == 6 && warps <= sms)
+        if (sum_stages == 7 || (sum_stages == 6 && warps <= sms))
             launch_ex(k_blocksum<6, 8>, dim3(warps), dim3(32), sum_smem<6, 8>(), stream, pdl_ok, tmap, n_slots,
-                      Q, plan.sym ? 1 : 0, pair_dirs, d_partials, d_tickets, d_out);
+                      Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
         else
             launch_ex(k_blocksum<3, 8>, dim3(warps), dim3(32), sum_smem<3, 8>(), stream, pdl_ok, tmap, n_slots,
-                      Q, plan.sym ? 1 : 0, pair_dirs, d_partials, d_tickets, d_out);
+                      Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
         if (prof) prof->end(stream);
         launches += 1;
         QC_CUDA(cudaGetLastError());
