@@ -790,13 +790,15 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             return e ? std::atoi(e) : 1;
         }();
         // L2 keep/drop hints on the two reads of each stored part (SYM): block sum at q = 22 /
-        // 24 / 26 118.6 -> 115.2, 176.8 -> 169.8, 261.4 -> 250.6 us per launch; at q = 20 (f
-        // fits L2) 38.5 -> 39.5, so on from Q = 21 stored bits. QCG_SUM_HINT=0/1 forces.
+        // 24 / 26 118.6 -> 115.2, 176.8 -> 169.8, 261.4 -> 250.6 us per launch; at q = 20 x 21
+        // slots (88 MB of f, L2-resident) 38.5 -> 39.5, so on when the launch's f exceeds
+        // 96 MB. QCG_SUM_HINT=0/1 forces.
         static const int sum_hint_env = [] {
             const char* e = std::getenv("QCG_SUM_HINT");
             return e ? std::atoi(e) : -1;
         }();
-        const int sum_hint = sum_hint_env >= 0 ? sum_hint_env : (Q >= 21 ? 1 : 0);
+        const double f_bytes = static_cast<double>(n_slots) * N * 8.0;
+        const int sum_hint = sum_hint_env >= 0 ? sum_hint_env : (f_bytes > 96.0 * (1 << 20) ? 1 : 0);
         const int sum_mode = (pair_dirs ? 1 : 0) | (sum_hint ? 2 : 0) | (sum_hint == 2 ? 4 : 0);
         static const int sum_stages = [] {
             const char* e = std::getenv("QCG_SUM_STAGES");
