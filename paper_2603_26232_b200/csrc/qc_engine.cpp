@@ -279,6 +279,7 @@ bool zero_copy_out() {
 void qc_engine::enqueue_chunk(const std::vector<DevGraph>& dg, const EvalPoint* pts, int n, int p,
                               uint32_t flags, size_t slot0, ChunkCtx& ctx) {
     const auto t_enq = std::chrono::steady_clock::now();
+    if (ctx.shared) flags |= F_BALGRID;
     ctx.n = n;
     ctx.flags = flags;
     if (n <= 0) return;
@@ -564,8 +565,10 @@ std::vector<OptimizeOut> optimize_batch(qc_engine* e, const std::vector<DevGraph
                 nstreams = static_cast<size_t>(std::min(4L, std::max(1L, std::strtol(env, nullptr, 10))));
             for (size_t k = 0; k + 1 < nstreams; ++k) QC_CUDA(cudaStreamWaitEvent(e->aux[k], ready, 0));
             QC_CUDA(cudaEventDestroy(ready));
-            for (size_t c = 0; c < nchunks; ++c)
+            for (size_t c = 0; c < nchunks; ++c) {
                 ctx(c).st = (c % nstreams) ? e->aux[c % nstreams - 1] : e->stream;
+                ctx(c).shared = nstreams > 1;
+            }
             // Ping-pong (QCG_PINGPONG=1): whole-GPU pass kernels of concurrently queued chunks
             // otherwise interleave launch by launch, so the chunks stay in phase, their block
             // sums finish together and the device idles through every chunk's host step.

@@ -85,6 +85,7 @@ struct ChunkCtx {
     uint32_t flags = 0;
     double* d_out = nullptr;
     cudaStream_t st = nullptr;  // stream the chunk runs on (null: the engine stream)
+    bool shared = false;        // other chunks run concurrently on other streams
     // lockstep ping-pong: `passes` is recorded after this chunk's last pass kernel (before
     // its block sum); the chunk's next step first waits on `wait_on` (the previous chunk's
     // `passes`), so chunks' pass chains alternate instead of interleaving launch by launch

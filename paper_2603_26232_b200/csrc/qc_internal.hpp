@@ -113,6 +113,7 @@ enum : uint32_t {
     F_NOLEVREG = 256u,  // pass B (v4) f pass: levels read after the refill (experiment)
     F_A7EARLY = 2048u,  // split-buffer pass A: release the output buffer right after its store
     F_WHT = 1024u,      // fp32 mode only: Walsh–Hadamard form of the RX mixer (qc_amp.cuh)
+    F_BALGRID = 4096u,  // chunks share the GPU: balanced pass grids (qc_pass.cu pass_grid)
 };
 
 // One high (gather) pass: 3 column bits (0,1,2) + kHighBits tile bits.

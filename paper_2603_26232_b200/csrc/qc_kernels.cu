@@ -398,8 +398,9 @@ __host__ __device__ constexpr size_t sum_stage_bytes() { return size_t{32} * 16 
 // stages in flight: 3 lets two warp-CTAs share an SM (launches of more warps than SMs);
 // a launch that fits one warp per SM uses 6 (each 32 KB tensor copy takes ~1 us in the
 // SM's TMA unit, so deeper lookahead hides it)
-template <int STAGES, int PARTS>
-constexpr size_t sum_smem() { return STAGES * sum_stage_bytes<PARTS>() + 1024 + STAGES * 8; }
+// W warps per CTA (each with its own ring and chains, exactly one 1-warp CTA's work)
+template <int STAGES, int PARTS, int W = 1>
+constexpr size_t sum_smem() { return W * (STAGES * sum_stage_bytes<PARTS>() + STAGES * 8) + 1024; }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -409,8 +410,8 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // part (128 B stride)}, box {16, 32, kSumParts}, 128-byte swizzle: the shared box is
 // [part][block][16 doubles] and 16-byte unit u of row r sits at unit u ^ (r & 7), so the
 // 32 lanes (one block each) read one part conflict-free.
-template <int kSumStages, int kSumParts>
-__global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtensorMap tmap,
+template <int kSumStages, int kSumParts, int kW = 1>
+__global__ void __launch_bounds__(32 * kW) k_blocksum(const __grid_constant__ CUtensorMap tmap,
                                                 int n_slots, int Q, int sym, int mode,
                                                 double* __restrict__ partials,
                                                 unsigned* __restrict__ tickets,
@@ -421,9 +422,11 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     extern __shared__ unsigned char sraw[];
     // 1024-byte aligned base by pointer arithmetic, so the compiler keeps the shared
     // address space (LDS instead of generic LD on the chain's operand path)
-    unsigned char* sbase = sraw + ((1024u - (smem_u32(sraw) & 1023u)) & 1023u);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sbase + kSumStages * kSumStageBytes);
-    const int lane = threadIdx.x;
+    unsigned char* const abase = sraw + ((1024u - (smem_u32(sraw) & 1023u)) & 1023u);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int vb = blockIdx.x * kW + wid;            // this warp's work unit
+    unsigned char* sbase = abase + wid * (kSumStages * kSumStageBytes);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(abase + kW * kSumStages * kSumStageBytes) + wid * kSumStages;
     const int nbl = 1 << (Q - 12);                   // stored blocks per slot
     const int chains = sym ? 2 * nbl : nbl;
     // direction-uniform warps: each covers up to 32 stored blocks in ONE direction (SYM:
@@ -431,9 +434,9 @@ __global__ void __launch_bounds__(32) k_blocksum(const __grid_constant__ CUtenso
     const int bpw = min(32, nbl);                    // blocks per warp
     const int wpd = nbl / bpw;                       // warps per direction per slot
     const int wps = sym ? 2 * wpd : wpd;             // warps per slot
-    const int slot = blockIdx.x / wps;
+    const int slot = vb / wps;
     if (slot >= n_slots) return;
-    const int wis = blockIdx.x - slot * wps;
+    const int wis = vb - slot * wps;
     // SYM: the ascending and the descending warp of a block group are adjacent CTAs, so
     // they run together and the second read of each stored block can hit L2 (at 24+ qubits
     // f does not fit in L2 and the sum is bound by its read stream)
@@ -726,7 +729,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
         // FP64: 6 per amplitude for the phase, 6 per amplitude per RX target (12 targets)
         const double oa = (nph * 6.0 + nmix * 72.0) * N;
         if (prof) prof->begin(K_PASS_LOW, ba, stream, oa);
-        launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok && l > 0,
+        launch_pass_a4(d_slots, d_lp, l, Q, fa | (flags & (F_FP32 | F_WHT | F_BALGRID)), n_slots, stream, pdl_ok && l > 0,
                        state_base);
         if (prof) prof->end(stream);
         ++launches;
@@ -745,7 +748,7 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             // 6 per amplitude per pair op (RX target or mirror), + |a|^2 C(z) (4) when f is emitted
             const double oh = nmix * 6.0 * items * N + ((fh & F_EXPECT) ? n_slots * 4.0 * N : 0.0);
             if (prof) prof->begin(K_PASS_HIGH, bh, stream, oh);
-            launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & (F_FP32 | F_WHT)), n_slots, stream, pdl_ok,
+            launch_pass_b4(d_slots, d_lp, l, Q, plan.high[h], fh | (flags & (F_FP32 | F_WHT | F_BALGRID)), n_slots, stream, pdl_ok,
                            state_base);
             if (prof) prof->end(stream);
             ++launches;
@@ -775,11 +778,25 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
                                          static_cast<int>(sum_smem<3, 8>())));
             QC_CUDA(cudaFuncSetAttribute(k_blocksum<6, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sum_smem<6, 8>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<3, 8, 2>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<3, 4, 4>())));
+            QC_CUDA(cudaFuncSetAttribute(k_blocksum<3, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(sum_smem<3, 2, 8>())));
         });
+        // Warps per CTA (QCG_SUM_WARPS = 1 | 2 | 4 | 8; stages of 8 / 8 / 4 / 2 parts): packs
+        // a launch's chains onto fewer SMs, leaving the rest to the other chunk's passes.
+        static const int sum_warps = [] {
+            const char* e = std::getenv("QCG_SUM_WARPS");
+            const int w = e ? std::atoi(e) : 1;
+            return (w == 2 || w == 4 || w == 8) ? w : 1;
+        }();
+        const int sum_parts = sum_warps == 4 ? 4 : sum_warps == 8 ? 2 : 8;
         // stages x 1 KB-per-lane chunks: 6 deep when every warp has an SM to itself, else
         // 3 (two warp-CTAs per SM). Smaller stages measured slower at every size
         // (profiles/r1_blocksum_stages.txt).
-        const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl, 8);
+        const CUtensorMap tmap = fbuf_tensor_map(d_fbuf, static_cast<uint64_t>(n_slots) * nbl, sum_parts);
         if (prof) prof->begin(K_BLOCKSUM, n_slots * N * 8.0, stream, n_slots * N * (plan.sym ? 2.0 : 1.0));
         // Ring depth: 3 stages (two warp-CTAs per SM) by default. With two chunk streams the
         // two chunks' block sums often run at once (C2: 80 + 88 warps > 148 SMs), and 6-stage
@@ -804,7 +821,17 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
             const char* e = std::getenv("QCG_SUM_STAGES");
             return e ? std::atoi(e) : 3;
         }();
-        if (sum_stages == 7 || (sum_stages == 6 && warps <= sms))
+        const unsigned wgrid = static_cast<unsigned>((warps + sum_warps - 1) / sum_warps);
+        if (sum_warps == 2)
+            launch_ex(k_blocksum<3, 8, 2>, dim3(wgrid), dim3(64), sum_smem<3, 8, 2>(), stream, pdl_ok, tmap,
+                      n_slots, Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
+        else if (sum_warps == 4)
+            launch_ex(k_blocksum<3, 4, 4>, dim3(wgrid), dim3(128), sum_smem<3, 4, 4>(), stream, pdl_ok, tmap,
+                      n_slots, Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
+        else if (sum_warps == 8)
+            launch_ex(k_blocksum<3, 2, 8>, dim3(wgrid), dim3(256), sum_smem<3, 2, 8>(), stream, pdl_ok, tmap,
+                      n_slots, Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
+        else if (sum_stages == 7 || (sum_stages == 6 && warps <= sms))
             launch_ex(k_blocksum<6, 8>, dim3(warps), dim3(32), sum_smem<6, 8>(), stream, pdl_ok, tmap, n_slots,
                       Q, plan.sym ? 1 : 0, sum_mode, d_partials, d_tickets, d_out);
         else

@@ -1343,15 +1343,26 @@ int sm_count() {
 // Slots per launch such that every CTA's contiguous tile range spans <= kDescCap slots
 // (a CTA spans at most slots/grid + 3).
 int slots_per_launch(int sms) { return (v4::kDescCap - 3) * sms; }
-// Persistent grid for `tiles` tiles of n slots: min(tiles, SMs). QCG_GRID=bal: the smallest
-// grid with the same number of group-tile rounds (two groups per CTA take alternate tiles),
-// leaving the other SMs to a concurrently queued chunk; measured on C2: 70.84 vs 71.22 ms
-// per solve, but each launch alone 5% slower (fewer SMs' bandwidth), so not the default.
-uint32_t pass_grid(uint32_t tiles, int n, int sms) {
-    static const bool full = [] {
+// Persistent grid for `tiles` tiles of n slots. Full grid: min(tiles, SMs). Balanced: the
+// smallest grid with the same number of group-tile rounds (two groups per CTA take
+// alternate tiles), leaving the other SMs to a concurrently queued chunk. Each launch alone
+// is slower with fewer SMs (C2 shape pass A 81 -> 85 us), but with two chunk streams the
+// other chunk's kernels start on the freed SMs at once: C2 67.6 -> 66.6 ms per solve
+// (tools/grid_bal.sh). So the engine asks for it (F_BALGRID) only when chunks share the
+// GPU. QCG_GRID=full|bal forces one; x2|x3: 2 or 3 CTA waves (measured slower, §4a (18)).
+uint32_t pass_grid(uint32_t tiles, int n, int sms, uint32_t flags) {
+    static const int gmode = [] {  // -1 auto, 0 full, 1 bal, k >= 2: k waves
         const char* e = std::getenv("QCG_GRID");
-        return !(e && std::string(e) == "bal");
+        if (e && std::string(e) == "bal") return 1;
+        if (e && std::string(e) == "full") return 0;
+        if (e && e[0] == 'x') return std::max(2, std::atoi(e + 1));
+        return -1;
     }();
+    const bool full = gmode == 0 || (gmode == -1 && !(flags & F_BALGRID));
+    if (gmode >= 2) {
+        const uint32_t g = std::min<uint32_t>(tiles, static_cast<uint32_t>(gmode * sms));
+        if (static_cast<uint32_t>(n) / std::max<uint32_t>(g, 1) + 3 <= static_cast<uint32_t>(v4::kDescCap)) return g;
+    }
     const uint32_t g0 = std::min<uint32_t>(tiles, static_cast<uint32_t>(sms));
     if (full || g0 == 0) return g0;
     const uint32_t rounds = (tiles + 2 * g0 - 1) / (2 * g0);
@@ -1445,7 +1456,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-            const uint32_t grid = pass_grid(tiles, n, sms);
+            const uint32_t grid = pass_grid(tiles, n, sms, flags);
             const CUtensorMap tm = state_tensor_map(
                 static_cast<const char*>(state_base) + (static_cast<size_t>(s0) << Q) * (fp32 ? 8 : 16),
                 static_cast<uint64_t>(n) << Q, fp32);
@@ -1483,7 +1494,7 @@ int launch_pass_a4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-        const uint32_t grid = pass_grid(tiles, n, sms);
+        const uint32_t grid = pass_grid(tiles, n, sms, flags);
         if (fp32)
             launch_ex(v4::k_pass_a<float2>, dim3(grid), dim3(v4::kThreads), v4::kSmem, stream,
                       pdl || s0 > 0, d_slots + s0, d_lp, layer, Q, flags, tiles);
@@ -1637,7 +1648,7 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
         for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
             const int n = std::min(n_slots - s0, slots_per_launch(sms));
             const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-            const uint32_t grid = pass_grid(tiles, n, sms);
+            const uint32_t grid = pass_grid(tiles, n, sms, flags);
             P.dims[4] = (1ull << P.geo.hi_bits) * static_cast<cuuint64_t>(n);
             CUtensorMap tm;
             const cuuint32_t es[5] = {1, 1, 1, 1, 1};
@@ -1665,7 +1676,7 @@ int launch_pass_b4(const SlotDesc* d_slots, const LayerParam* d_lp, int layer, i
     for (int s0 = 0; s0 < n_slots; s0 += slots_per_launch(sms)) {
         const int n = std::min(n_slots - s0, slots_per_launch(sms));
         const uint32_t tiles = static_cast<uint32_t>(n) << (Q - 12);
-        const uint32_t grid = pass_grid(tiles, n, sms);
+        const uint32_t grid = pass_grid(tiles, n, sms, flags);
         static const uint32_t nolev = [] {
             const char* e = std::getenv("QCG_LEVREG");
             return (e && e[0] == '0') ? static_cast<uint32_t>(F_NOLEVREG) : 0u;
