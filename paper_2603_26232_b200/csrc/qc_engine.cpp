@@ -64,6 +64,49 @@ HostBuf::~HostBuf() {
     if (p) cudaFreeHost(p);
 }
 
+namespace {
+// Parallel form of the validation loop below for large edge lists (C4: 9.3M edges, C5:
+// 12.8M; the serial loop took ~65 ms of C4's end-to-end step): threads take contiguous edge
+// ranges, the duplicate bitset is updated with atomic fetch-or. Any problem (range,
+// self-loop, weight, duplicate) returns false and the serial loop re-runs to raise exactly
+// the reference's first error; the weight total is summed in edge order as there.
+bool load_graph_parallel(const qc_graph* g, HostGraph& h, uint64_t nn, int threads) {
+    const int m = g->m;
+    h.u.resize(static_cast<size_t>(m));
+    h.v.resize(static_cast<size_t>(m));
+    h.w.resize(static_cast<size_t>(m));
+    std::vector<uint64_t> bits(static_cast<size_t>((nn * nn / 2 + nn) / 64 + 1), 0);
+    int bad = 0, nonint = 0;
+    const uint32_t n = static_cast<uint32_t>(g->n);
+#pragma omp parallel for schedule(static) num_threads(threads) reduction(| : bad, nonint)
+    for (int i = 0; i < m; ++i) {
+        uint32_t u = g->edges[i].u, v = g->edges[i].v;
+        const double w = g->edges[i].w;
+        if (u >= n || v >= n || u == v || w < 0.0 || std::isnan(w)) {
+            bad = 1;
+            continue;
+        }
+        if (u > v) std::swap(u, v);
+        const uint64_t k = static_cast<uint64_t>(u) * (2 * nn - u - 1) / 2 + (v - u - 1);
+        const uint64_t bit = uint64_t{1} << (k & 63);
+        if (__atomic_fetch_or(&bits[k >> 6], bit, __ATOMIC_RELAXED) & bit) {
+            bad = 1;
+            continue;
+        }
+        h.u[static_cast<size_t>(i)] = u;
+        h.v[static_cast<size_t>(i)] = v;
+        h.w[static_cast<size_t>(i)] = w;
+        if (w != std::floor(w)) nonint = 1;
+    }
+    if (bad) return false;
+    double total = 0.0;
+    for (int i = 0; i < m; ++i) total += h.w[static_cast<size_t>(i)];
+    h.total = total;
+    h.integral = !nonint;
+    return true;
+}
+}  // namespace
+
 // graph.hpp:37-50 Graph::add_edge validation; statevector.hpp:83-89 integrality.
 HostGraph load_graph(const qc_graph* g) {
     if (!g) config_error("null graph");
@@ -79,6 +122,16 @@ HostGraph load_graph(const qc_graph* g) {
     // pair u < v when that fits in 64 MB (n <= ~32k: every BASELINE config), else a hash set
     const uint64_t nn = static_cast<uint64_t>(g->n);
     const bool use_bits = nn * nn / 2 <= (uint64_t{64} << 23);
+    const int par = std::min(16, static_cast<int>(std::max(1u, std::thread::hardware_concurrency())));
+    if (use_bits && g->m >= (1 << 18) && par > 1) {
+        if (load_graph_parallel(g, h, nn, par)) {
+            h.all_int = h.integral && h.total <= 4.0e18;
+            if (h.total > 65535.0) h.integral = false;
+            return h;
+        }
+        h = HostGraph{};  // a problem: the serial pass raises the reference's first error
+        h.n = g->n;
+    }
     std::vector<uint64_t> bits;
     std::unordered_set<uint64_t> keys;
     if (use_bits)

@@ -182,3 +182,56 @@ def test_product_generators_match_oracle(oracle):
     deg = np.bincount(np.concatenate([g["u"], g["v"]]), minlength=1000)
     assert (deg == 3).all() and (g["u"] < g["v"]).all()
     assert set(np.unique(g["w"])) <= set(float(x) for x in range(1, 11))
+
+
+def _big_edges(n=3000, m=400_000, seed=5):
+    """m distinct (u < v) pairs over n vertices as an EDGE_DTYPE array (integer weights)."""
+    from paper_2603_26232_b200 import EDGE_DTYPE
+    rng = np.random.default_rng(seed)
+    keys = np.unique(rng.integers(0, n * (n - 1) // 2, size=int(m * 1.2)))[:m]
+    rng.shuffle(keys)
+    # index k of the row-major upper triangle -> (u, v)
+    u = (n - 2 - np.floor(np.sqrt(-8 * keys + 4 * n * (n - 1) - 7) / 2.0 - 0.5)).astype(np.int64)
+    v = keys + u + 1 - n * (n - 1) // 2 + (n - u) * ((n - u) - 1) // 2
+    e = np.zeros(len(keys), dtype=EDGE_DTYPE)
+    e["u"], e["v"], e["w"] = u, v, rng.integers(1, 4, size=len(keys)).astype(np.float64)
+    flip = rng.random(len(keys)) < 0.5
+    e["u"][flip], e["v"][flip] = v[flip], u[flip]
+    return e
+
+
+def _load_error(n, e):
+    from paper_2603_26232_b200 import QcError, run_record_bytes
+    try:
+        run_record_bytes(n, e, qubit_cap=20, layers=1, top_k=2)
+    except QcError as ex:
+        return str(ex)
+    return None
+
+
+def test_large_graph_validation_first_error():
+    """load_graph's parallel validation (m >= 2^18) accepts a valid large edge list and, on any
+    problem, reports exactly the first error in edge order as graph.hpp:37-50 add_edge does
+    (qc_engine.cpp load_graph falls back to the serial loop)."""
+    n = 3000
+    e = _big_edges(n)
+    assert len(e) == 400_000 and np.all(e["u"] != e["v"])
+    assert _load_error(n, e) is None
+    # a duplicate late in the list, then a self-loop after it: the duplicate is reported
+    d = e.copy()
+    d[350_000] = (d[10]["v"], d[10]["u"], 1.0)
+    d[390_000] = (7, 7, 1.0)
+    lo, hi = sorted((int(d[10]["u"]), int(d[10]["v"])))
+    assert f"duplicate edge ({lo},{hi})" in _load_error(n, d)
+    # the self-loop first: it is reported
+    d2 = e.copy()
+    d2[300_000] = (7, 7, 1.0)
+    d2[350_000] = (d2[10]["v"], d2[10]["u"], 1.0)
+    assert "self-loop rejected at vertex 7" in _load_error(n, d2)
+    # out-of-range endpoint and negative weight
+    d3 = e.copy()
+    d3[200_000] = (1, n, 1.0)
+    assert "out of range" in _load_error(n, d3)
+    d4 = e.copy()
+    d4[399_999]["w"] = -1.0
+    assert "negative or NaN" in _load_error(n, d4)
