@@ -716,7 +716,10 @@ int launch_chain(const ChainPlan& plan, const SlotDesc* d_slots, const LayerPara
     // of this chain (the first one follows the staging copy). Off by default: with two
     // chunk streams the early-scheduled dependent CTAs hold SMs the other stream's kernels
     // need (C2: 82.8 ms/solve with PDL vs 75.6 without). QCG_PDL=1 enables it.
-    static const bool pdl_ok = std::getenv("QCG_PDL") != nullptr;
+    static const bool pdl_ok = [] {
+        const char* e = std::getenv("QCG_PDL");
+        return e && e[0] == '1';
+    }();
     for (int l = 0; l < p; ++l) {
         const uint32_t fa = (l == 0 && (flags & F_INIT)) ? F_INIT : 0u;
         const int nph = cnt(stats ? &stats->phase : nullptr, l);
